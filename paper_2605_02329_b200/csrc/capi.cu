@@ -1,0 +1,764 @@
+// capi.cu — the C-ABI of include/slosim_b200.h: host entry points, device
+// workspace management and the single-snapshot kernels (K7) that expose the
+// policies and cost models of the engine one decision at a time.  The snapshot
+// kernels call the very same device functions as the batched engine.
+#include <cuda_runtime.h>
+#include <math.h>
+#include <stdio.h>
+#include <string.h>
+
+#include <algorithm>
+#include <mutex>
+#include <vector>
+
+#include "engine.cuh"
+
+using namespace slosim;
+
+namespace {
+
+thread_local char g_err[512];
+std::mutex g_mu;
+
+int fail_cuda(cudaError_t e, const char* what) {
+    snprintf(g_err, sizeof(g_err), "%s: %s", what, cudaGetErrorString(e));
+    return SLOSIM_ECUDA;
+}
+
+#define CK(call)                                              \
+    do {                                                      \
+        cudaError_t e_ = (call);                              \
+        if (e_ != cudaSuccess) return fail_cuda(e_, #call);   \
+    } while (0)
+
+// Grow-only device arena per purpose (the engine workspace, profile tables, snapshot scratch).
+struct Arena {
+    void* ptr = nullptr;
+    size_t size = 0;
+    int device = -1;
+    cudaError_t reserve(size_t bytes) {
+        int dev = 0;
+        cudaGetDevice(&dev);
+        if (ptr && size >= bytes && dev == device) return cudaSuccess;
+        if (ptr && dev == device) cudaFree(ptr);
+        ptr = nullptr;
+        size = 0;
+        size_t want = std::max(bytes, (size_t)1 << 20);
+        cudaError_t e = cudaMalloc(&ptr, want);
+        if (e != cudaSuccess) { ptr = nullptr; return e; }
+        size = want;
+        device = dev;
+        return cudaSuccess;
+    }
+};
+Arena g_ws, g_tabs, g_work, g_snap;
+
+int g_sms = 0, g_blocks_per_sm = 0;
+
+int launch_geometry(int64_t n_instances, int* grid) {
+    if (!g_sms) {
+        int dev = 0;
+        CK(cudaGetDevice(&dev));
+        CK(cudaDeviceGetAttribute(&g_sms, cudaDevAttrMultiProcessorCount, dev));
+        CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&g_blocks_per_sm, sim_kernel, 128, 0));
+        if (g_blocks_per_sm < 1) g_blocks_per_sm = 1;
+    }
+    int64_t warps_needed = n_instances;
+    int64_t blocks = (warps_needed + 3) / 4;
+    int64_t full = (int64_t)g_sms * g_blocks_per_sm;
+    *grid = (int)std::max<int64_t>(1, std::min<int64_t>(blocks, full));
+    return SLOSIM_OK;
+}
+
+}  // namespace
+
+// ------------------------------------------------------------------ engine --
+extern "C" int64_t slosim_workspace_bytes(const slosim_batch_t* b) {
+    if (!b) return -1;
+    int grid = 0;
+    if (launch_geometry(b->n_instances, &grid) != SLOSIM_OK) return -1;
+    return (int64_t)grid * 4 * (int64_t)ws_bytes(b->max_requests) +
+           (int64_t)b->n_profiles * 2 * (int64_t)sizeof(ProfTab);
+}
+
+extern "C" int slosim_run_batch(const slosim_batch_t* b, void* stream) {
+    if (!b || b->n_instances < 0 || b->n_profiles < 1 || !b->profiles || !b->instances || !b->summaries)
+        return SLOSIM_EINVAL;
+    if (b->n_instances == 0) return SLOSIM_OK;
+    if ((b->flags & SLOSIM_F_ROWS) &&
+        (!b->rows.ttft_us || !b->rows.mean_tpot_us || !b->rows.decode_tps || !b->rows.met_flags ||
+         !b->rows.deadline_misses || !b->rows.t_prefill_finish || !b->rows.t_first_token ||
+         !b->rows.t_last_token || !b->rows.first_sched_us))
+        return SLOSIM_EINVAL;
+    if ((b->flags & SLOSIM_F_EXPORT_LUT) && (!b->lut_out_sums || !b->lut_out_counts)) return SLOSIM_EINVAL;
+    cudaStream_t st = (cudaStream_t)stream;
+    std::lock_guard<std::mutex> lock(g_mu);
+    int64_t cap = b->max_requests;
+    if (cap <= 0) {
+        std::vector<slosim_instance_t> h((size_t)b->n_instances);
+        CK(cudaMemcpyAsync(h.data(), b->instances, h.size() * sizeof(slosim_instance_t), cudaMemcpyDeviceToHost, st));
+        CK(cudaStreamSynchronize(st));
+        for (auto& x : h) cap = std::max<int64_t>(cap, x.n_requests);
+    }
+    int grid = 0;
+    int rc = launch_geometry(b->n_instances, &grid);
+    if (rc) return rc;
+    size_t stride = ws_bytes(cap);
+    size_t total = stride * (size_t)grid * 4;
+    CK(g_ws.reserve(total));
+    CK(g_tabs.reserve(sizeof(ProfTab) * 2 * (size_t)b->n_profiles));
+    CK(g_work.reserve(64));
+    ProfTab* sched = (ProfTab*)g_tabs.ptr;
+    ProfTab* frozen = sched + b->n_profiles;
+    build_profile_tables<<<b->n_profiles, 32, 0, st>>>(b->profiles, b->n_profiles, sched, frozen);
+    CK(cudaGetLastError());
+    CK(cudaMemsetAsync(g_work.ptr, 0, 8, st));
+    Ctx cx;
+    cx.B = *b;
+    cx.sched_tab = sched;
+    cx.frozen_tab = frozen;
+    sim_kernel<<<grid, 128, 0, st>>>(cx, (char*)g_ws.ptr, stride, cap, (unsigned long long*)g_work.ptr);
+    CK(cudaGetLastError());
+    return SLOSIM_OK;
+}
+
+namespace {
+template <class T>
+cudaError_t up(T** d, const T* h, size_t n, std::vector<void*>& owned) {
+    *d = nullptr;
+    if (!h || n == 0) return cudaSuccess;
+    cudaError_t e = cudaMalloc((void**)d, n * sizeof(T));
+    if (e != cudaSuccess) return e;
+    owned.push_back(*d);
+    return cudaMemcpy(*d, h, n * sizeof(T), cudaMemcpyHostToDevice);
+}
+template <class T>
+cudaError_t alloc(T** d, size_t n, std::vector<void*>& owned) {
+    *d = nullptr;
+    if (n == 0) return cudaSuccess;
+    cudaError_t e = cudaMalloc((void**)d, n * sizeof(T));
+    if (e == cudaSuccess) owned.push_back(*d);
+    return e;
+}
+struct Owned {
+    std::vector<void*> v;
+    ~Owned() { for (void* p : v) cudaFree(p); }
+};
+}  // namespace
+
+extern "C" int slosim_run_batch_host(const slosim_batch_t* hb, float* elapsed_ms) {
+    if (!hb) return SLOSIM_EINVAL;
+    Owned o;
+    slosim_batch_t d = *hb;
+    size_t nt = (size_t)hb->traces.n_total, ni = (size_t)hb->n_instances;
+    int64_t rows_n = 0, tb_n = 0;
+    for (size_t i = 0; i < ni; i++) {
+        const slosim_instance_t& x = hb->instances[i];
+        rows_n = std::max<int64_t>(rows_n, x.row_offset + x.n_requests);
+        if (x.trace_buf_offset >= 0) tb_n = std::max<int64_t>(tb_n, x.trace_buf_offset + x.trace_buf_words);
+        d.max_requests = std::max<int64_t>(d.max_requests, x.n_requests);
+    }
+    CK(up((int64_t**)&d.traces.arrival_us, hb->traces.arrival_us, nt, o.v));
+    CK(up((int32_t**)&d.traces.input_len, hb->traces.input_len, nt, o.v));
+    CK(up((int32_t**)&d.traces.output_len, hb->traces.output_len, nt, o.v));
+    CK(up((int32_t**)&d.traces.prefix_hit_len, hb->traces.prefix_hit_len, nt, o.v));
+    CK(up((int32_t**)&d.traces.id_rank, hb->traces.id_rank, nt, o.v));
+    CK(up((slosim_profile_t**)&d.profiles, hb->profiles, (size_t)hb->n_profiles, o.v));
+    CK(up((slosim_instance_t**)&d.instances, hb->instances, ni, o.v));
+    CK(alloc(&d.summaries, ni, o.v));
+    bool rows = (hb->flags & SLOSIM_F_ROWS) != 0;
+    size_t rn = rows ? (size_t)rows_n : 0;
+    CK(alloc(&d.rows.ttft_us, rn, o.v)); CK(alloc(&d.rows.mean_tpot_us, rn, o.v));
+    CK(alloc(&d.rows.decode_tps, rn, o.v)); CK(alloc(&d.rows.met_flags, rn, o.v));
+    CK(alloc(&d.rows.deadline_misses, rn, o.v)); CK(alloc(&d.rows.t_prefill_finish, rn, o.v));
+    CK(alloc(&d.rows.t_first_token, rn, o.v)); CK(alloc(&d.rows.t_last_token, rn, o.v));
+    CK(alloc(&d.rows.first_sched_us, rn, o.v));
+    size_t tbn = hb->trace_buf ? (size_t)tb_n : 0;
+    CK(alloc(&d.trace_buf, tbn, o.v));
+    if (!hb->trace_buf) d.trace_buf = nullptr;
+    const size_t FR = SLOSIM_MAX_BSZ_BUCKETS * SLOSIM_MAX_SEQ_BUCKETS;
+    bool lut = (hb->flags & SLOSIM_F_EXPORT_LUT) && hb->lut_out_sums;
+    CK(alloc(&d.lut_out_sums, lut ? ni * FR : 0, o.v));
+    CK(alloc(&d.lut_out_counts, lut ? ni * FR : 0, o.v));
+    cudaEvent_t e0, e1;
+    CK(cudaEventCreate(&e0));
+    CK(cudaEventCreate(&e1));
+    CK(cudaEventRecord(e0, 0));
+    int rc = slosim_run_batch(&d, nullptr);
+    CK(cudaEventRecord(e1, 0));
+    CK(cudaEventSynchronize(e1));
+    if (elapsed_ms) cudaEventElapsedTime(elapsed_ms, e0, e1);
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+    if (rc) return rc;
+    CK(cudaMemcpy(hb->summaries, d.summaries, ni * sizeof(slosim_summary_t), cudaMemcpyDeviceToHost));
+    if (rows) {
+        const slosim_rows_t& R = hb->rows;
+#define COPYROW(f, T) if (R.f) CK(cudaMemcpy(R.f, d.rows.f, rn * sizeof(T), cudaMemcpyDeviceToHost))
+        COPYROW(ttft_us, int64_t); COPYROW(mean_tpot_us, double); COPYROW(decode_tps, double);
+        COPYROW(met_flags, uint8_t); COPYROW(deadline_misses, int32_t); COPYROW(t_prefill_finish, int64_t);
+        COPYROW(t_first_token, int64_t); COPYROW(t_last_token, int64_t); COPYROW(first_sched_us, int64_t);
+#undef COPYROW
+    }
+    if (tbn) CK(cudaMemcpy(hb->trace_buf, d.trace_buf, tbn * sizeof(int64_t), cudaMemcpyDeviceToHost));
+    if (lut) {
+        CK(cudaMemcpy(hb->lut_out_sums, d.lut_out_sums, ni * FR * sizeof(double), cudaMemcpyDeviceToHost));
+        CK(cudaMemcpy(hb->lut_out_counts, d.lut_out_counts, ni * FR * sizeof(int32_t), cudaMemcpyDeviceToHost));
+    }
+    return SLOSIM_OK;
+}
+
+// ------------------------------------------------------- snapshot kernels --
+namespace {
+
+// A framed LUT table in device scratch, built by one warp (lane = row).
+__device__ void snap_build_lut(int nb, int ns, const int32_t* bb, const int32_t* sb, const double* fsums,
+                               const int32_t* fcounts, ProfTab* tab, int lane) {
+    uint32_t rm = 0;
+    build_lut_table(nb, ns, bb, sb, fsums, fcounts, tab->sum, tab->mean, tab->slope, tab->cnt, tab->colmask, &rm,
+                    lane);
+    if (lane == 0) { tab->rowmask = rm; tab->empty = rm == 0; }
+    __syncwarp();
+}
+
+struct SnapLut {
+    int nb, ns;
+    int32_t bb[SLOSIM_MAX_BSZ_BUCKETS];
+    int32_t sb[SLOSIM_MAX_SEQ_BUCKETS];
+};
+
+__global__ void k_lut_lookup(SnapLut sl, const double* fsums, const int32_t* fcounts, ProfTab* tab, int64_t n,
+                             const int64_t* bsz, const int64_t* seq, double* out) {
+    __shared__ SnapLut s;
+    if (threadIdx.x == 0) s = sl;
+    __syncthreads();
+    if (threadIdx.x < 32) snap_build_lut(s.nb, s.ns, s.bb, s.sb, fsums, fcounts, tab, threadIdx.x);
+    __syncthreads();
+    __threadfence_block();
+    DLut L{s.nb, s.ns, s.bb, s.sb, tab->sum, tab->mean, tab->slope, tab->cnt, tab->colmask, tab->rowmask};
+    for (int64_t k = threadIdx.x; k < n; k += blockDim.x) out[k] = lut_lookup(L, bsz[k], seq[k]);
+}
+
+__global__ void k_formula(int nbase, const int64_t* bx, const double* by, double gamma, int64_t n, const int64_t* bsz,
+                          const int64_t* seq, double* out) {
+    int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (k < n) out[k] = decode_formula(nbase, bx, by, gamma, bsz[k], seq[k]);
+}
+
+__global__ void k_estimate(int64_t tok, int64_t busy, int64_t n, const int64_t* tokens, int64_t* out) {
+    int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (k < n) out[k] = ceil_muldiv(tokens[k], busy, tok);
+}
+
+__global__ void k_predict(int n, const int64_t* arr, const int64_t* rem, int64_t t_now, int64_t tok, int64_t busy,
+                          int64_t* out) {
+    int lane = threadIdx.x;
+    int64_t cursor = t_now;
+    for (int base = 0; base < n; base += 32) {
+        int k = base + lane;
+        bool v = k < n;
+        int64_t a = v ? arr[k] : 0;
+        int64_t d = v ? ceil_muldiv(rem[k], busy, tok) : 0;
+        int nvalid = n - base < 32 ? n - base : 32;
+        int64_t fin = fcfs_walk_chunk(v, a, d, cursor, nvalid, lane);
+        if (v) out[k] = fin;
+    }
+}
+
+// Sort snapshot entries by (arrival, id_rank) into a queue workspace (one warp).
+__device__ void snap_queue(int n, const int64_t* arr, const int32_t* inp, const int64_t* rem, const int32_t* idr,
+                           const WS& w, int lane) {
+    for (int i0 = 0; i0 < n; i0 += 32) {
+        int i = i0 + lane;
+        int rank = 0;
+        if (i < n) {
+            for (int j = 0; j < n; j++) {
+                bool less = arr[j] < arr[i] || (arr[j] == arr[i] && idr[j] < idr[i]);
+                rank += less;
+            }
+            w.q_pos[rank] = i;
+            w.q_arr[rank] = arr[i];
+            w.q_inp[rank] = inp[i];
+            w.q_rem[rank] = (int32_t)rem[i];
+            w.q_full[rank] = (int32_t)rem[i];
+        }
+    }
+    __syncwarp();
+}
+
+__global__ void k_select_prefill(int policy, int n, const int64_t* arr, const int32_t* inp, const int64_t* rem,
+                                 const int32_t* idr, int64_t budget, int64_t t_now, int64_t tok, int64_t busy,
+                                 int64_t ttft, char* wsb, int64_t cap, int32_t* out_index, int64_t* out_take,
+                                 int32_t* n_out, double* out_scores) {
+    int lane = threadIdx.x;
+    WS w = carve_ws(wsb, cap);
+    snap_queue(n, arr, inp, rem, idr, w, lane);
+    int k = prefill_select(policy, w, 0, n, budget, t_now, tok, busy, ttft, w.pf_qidx, w.pf_take, lane);
+    for (int e = lane; e < k; e += 32) { out_index[e] = w.q_pos[w.pf_qidx[e]]; out_take[e] = w.pf_take[e]; }
+    if (policy == SLOSIM_PREFILL_KAIROS_URGENCY && out_scores)
+        for (int q = lane; q < n; q += 32) out_scores[w.q_pos[q]] = w.q_score[q];
+    if (lane == 0) *n_out = k;
+}
+
+__global__ void k_select_decode(int policy, int n, const int64_t* seq, const int32_t* idr, const int64_t* ngen,
+                                const double* tfirst, double t_now, int64_t tpot, SnapLut sl, const double* fsums,
+                                const int32_t* fcounts, ProfTab* tab, char* wsb, int64_t cap, int32_t* out_batch,
+                                int32_t* n_batch, int32_t* out_delayed, int32_t* n_delayed, double* out_times,
+                                double* out_pred, double* out_smin, int32_t* out_fb) {
+    __shared__ SnapLut s;
+    int lane = threadIdx.x;
+    if (lane == 0) s = sl;
+    __syncwarp();
+    snap_build_lut(s.nb, s.ns, s.bb, s.sb, fsums, fcounts, tab, lane);
+    DLut L{s.nb, s.ns, s.bb, s.sb, tab->sum, tab->mean, tab->slope, tab->cnt, tab->colmask, tab->rowmask};
+    WS w = carve_ws(wsb, cap);
+    int64_t mx = 0;
+    for (int i = lane; i < n; i += 32) {
+        w.a_seq[i] = (int32_t)seq[i];
+        w.a_idr[i] = idr[i];
+        w.a_flag[i] = 0;
+        mx = seq[i] > mx ? seq[i] : mx;
+    }
+    mx = wmax64(mx);
+    __syncwarp();
+    decode_order(n, w.a_seq, w.a_idr, w.a_ord, lane);
+    double fallback = lut_lookup(L, n, mx);
+    if (policy == SLOSIM_DECODE_CONTINUOUS) {
+        for (int r = lane; r < n; r += 32) out_batch[r] = w.a_ord[r];
+        if (lane == 0) {
+            *n_batch = n; *n_delayed = 0; *out_pred = fallback;
+            *out_smin = __longlong_as_double(0x7ff0000000000000LL);
+            *out_fb = 0;
+        }
+        return;
+    }
+    // compute_slack with the full-batch step cost (decode_sched.py:36-57, :75-79), f64 times
+    double smin = __longlong_as_double(0x7ff0000000000000LL);
+    for (int i = lane; i < n; i += 32) {
+        double sl2 = xsub(xsub((double)(tpot * (ngen[i] + 1)), xsub(t_now, tfirst[i])), fallback);
+        smin = sl2 < smin ? sl2 : smin;
+    }
+#pragma unroll
+    for (int o = 16; o; o >>= 1) { double x = __shfl_xor_sync(FULLMASK, smin, o); smin = x < smin ? x : smin; }
+    double tcur;
+    int64_t ms;
+    int nd = 0;
+    int b = decode_scan(L, n, w.a_ord, w.a_seq, w.a_flag, smin, &tcur, &ms, out_batch, out_delayed, out_times, &nd,
+                        lane);
+    __syncwarp();
+    if (b == 0) {
+        for (int r = lane; r < n; r += 32) out_batch[r] = w.a_ord[r];
+        if (lane == 0) { *n_batch = n; *n_delayed = 0; *out_pred = fallback; *out_smin = smin; *out_fb = 1; }
+    } else if (lane == 0) {
+        *n_batch = b; *n_delayed = nd; *out_pred = tcur; *out_smin = smin; *out_fb = 0;
+    }
+}
+
+__global__ void k_prefill_gt(int nc, const int64_t* cx, const int64_t* cy, int k, const int64_t* done,
+                             const int64_t* take, int64_t* out) {
+    __shared__ int64_t sx[SLOSIM_MAX_CURVE_POINTS], sy[SLOSIM_MAX_CURVE_POINTS];
+    if (threadIdx.x < nc) { sx[threadIdx.x] = cx[threadIdx.x]; sy[threadIdx.x] = cy[threadIdx.x]; }
+    __syncthreads();
+    if (threadIdx.x != 0) return;
+    double total = 0.0;
+    for (int e = 0; e < k; e++)
+        total = xadd(total, xsub(curve_at(nc, sx, sy, done[e] + take[e]), curve_at(nc, sx, sy, done[e])));
+    int64_t d = rint_i64(total);
+    *out = d < 1 ? 1 : d;
+}
+
+__global__ void k_request_metrics(int64_t n, const int64_t* arr, const int64_t* outl, const int64_t* off,
+                                  const int64_t* ts, int64_t ttft_slo, int64_t tpot_slo, int64_t* ttft, double* tpot,
+                                  double* tps, uint8_t* flags, int32_t* misses) {
+    int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (k >= n) return;
+    const int64_t* tk = ts + off[k];
+    int64_t m = off[k + 1] - off[k];
+    int64_t tf = tk[0];
+    int64_t v = tf - arr[k];
+    bool tm = v <= ttft_slo;
+    double tp = 0.0, tr = __longlong_as_double(0x7ff8000000000000LL);
+    bool pm = true;
+    if (outl[k] != 1) {
+        int64_t span = tk[m - 1] - tf;
+        tp = idiv(span, outl[k] - 1);
+        pm = tp <= (double)tpot_slo;
+        tr = xdiv((double)(outl[k] - 1), xdiv((double)span, 1e6));
+    }
+    int32_t mi = 0;
+    for (int64_t j = 1; j < m; j++) mi += tk[j] > tf + j * tpot_slo;
+    ttft[k] = v; tpot[k] = tp; tps[k] = tr;
+    flags[k] = (uint8_t)((tm ? 1 : 0) | (pm ? 2 : 0) | ((tm && pm) ? 4 : 0));
+    misses[k] = mi;
+}
+
+__global__ void k_aggregate(int64_t n, const uint8_t* flags, const double* tps, double* scratch, double* agg) {
+    int lane = threadIdx.x;
+    int64_t c0 = 0, c1 = 0, c2 = 0;
+    int cnt = 0;
+    for (int64_t base = 0; base < n; base += 32) {
+        int64_t k = base + lane;
+        bool v = k < n;
+        uint8_t f = v ? flags[k] : 0;
+        c0 += f & 1; c1 += (f >> 1) & 1; c2 += (f >> 2) & 1;
+        bool has = v && tps[k] == tps[k];
+        unsigned m = __ballot_sync(FULLMASK, has);
+        if (has) scratch[cnt + __popc(m & ((1u << lane) - 1u))] = tps[k];
+        cnt += __popc(m);
+    }
+    c0 = wsum64(c0); c1 = wsum64(c1); c2 = wsum64(c2);
+    __syncwarp();
+    double p50 = __longlong_as_double(0x7ff8000000000000LL), p90 = p50;
+    if (cnt > 0) {
+        int64_t r50 = (int64_t)ceil(xmul(50 / 100.0, (double)cnt));
+        int64_t r90 = (int64_t)ceil(xmul(90 / 100.0, (double)cnt));
+        p50 = radix_select(scratch, cnt, r50 < 1 ? 1 : r50, lane);
+        p90 = radix_select(scratch, cnt, r90 < 1 ? 1 : r90, lane);
+    }
+    if (lane == 0) {
+        agg[0] = idiv(c0, n); agg[1] = idiv(c1, n); agg[2] = idiv(c2, n); agg[3] = p50; agg[4] = p90;
+    }
+}
+
+__global__ void k_synth(slosim_profile_t* P, int na, const int64_t* ab, const int64_t* as, const double* aus,
+                        double gamma, int64_t w) {
+    __shared__ int64_t bx[SLOSIM_MAX_BASE_POINTS];
+    __shared__ double by[SLOSIM_MAX_BASE_POINTS];
+    __shared__ int nbase;
+    if (threadIdx.x == 0) {
+        // base = sorted((seq, float(us)) for bsz == 1)  (costmodel.py:290)
+        int m = 0;
+        for (int k = 0; k < na; k++) {
+            if (ab[k] != 1) continue;
+            int b = m++;
+            while (b > 0 && (bx[b - 1] > as[k] || (bx[b - 1] == as[k] && by[b - 1] > aus[k]))) {
+                bx[b] = bx[b - 1]; by[b] = by[b - 1]; b--;
+            }
+            bx[b] = as[k]; by[b] = aus[k];
+        }
+        nbase = m;
+    }
+    __syncthreads();
+    const int FR = SLOSIM_MAX_BSZ_BUCKETS * SLOSIM_MAX_SEQ_BUCKETS;
+    for (int c = threadIdx.x; c < FR; c += blockDim.x) {
+        int i = c / SLOSIM_MAX_SEQ_BUCKETS, j = c % SLOSIM_MAX_SEQ_BUCKETS;
+        double s = 0.0;
+        int32_t n = 0;
+        if (i < P->nb && j < P->ns && w != 0) {
+            // round(decode_step_formula(...)) then max(1, .) (costmodel.py:301-304)
+            int64_t v = rint_i64(decode_formula(nbase, bx, by, gamma, P->bsz_buckets[i], P->seq_buckets[j]));
+            if (v < 1) v = 1;
+            s = (double)(v * w);
+            n = (int32_t)w;
+        }
+        P->lut_sums[c] = s;
+        P->lut_counts[c] = n;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0 && w != 0) {
+        // anchors pinned in order (costmodel.py:305-308)
+        for (int k = 0; k < na; k++) {
+            int i = bucket_index(P->bsz_buckets, P->nb, ab[k]), j = bucket_index(P->seq_buckets, P->ns, as[k]);
+            P->lut_sums[i * SLOSIM_MAX_SEQ_BUCKETS + j] = xmul(aus[k], (double)w);
+            P->lut_counts[i * SLOSIM_MAX_SEQ_BUCKETS + j] = (int32_t)w;
+        }
+    }
+}
+
+// Snapshot scratch: carve typed buffers from one grow-only allocation.
+struct Bump {
+    char* base;
+    size_t off = 0;
+    template <class T>
+    T* take(size_t n) {
+        T* p = (T*)(base + off);
+        off += (n * sizeof(T) + 255) & ~(size_t)255;
+        return p;
+    }
+};
+
+cudaError_t snap_reserve(size_t bytes) { return g_snap.reserve(bytes); }
+
+SnapLut make_snaplut(int32_t nb, const int32_t* bb, int32_t ns, const int32_t* sb) {
+    SnapLut s{};
+    s.nb = nb; s.ns = ns;
+    for (int i = 0; i < nb; i++) s.bb[i] = bb[i];
+    for (int j = 0; j < ns; j++) s.sb[j] = sb[j];
+    return s;
+}
+
+void frame(int32_t nb, int32_t ns, const double* sums, const int32_t* counts, std::vector<double>& fs,
+           std::vector<int32_t>& fc) {
+    const size_t FR = SLOSIM_MAX_BSZ_BUCKETS * SLOSIM_MAX_SEQ_BUCKETS;
+    fs.assign(FR, 0.0);
+    fc.assign(FR, 0);
+    for (int i = 0; i < nb; i++)
+        for (int j = 0; j < ns; j++) {
+            fs[i * SLOSIM_MAX_SEQ_BUCKETS + j] = sums[i * ns + j];
+            fc[i * SLOSIM_MAX_SEQ_BUCKETS + j] = counts[i * ns + j];
+        }
+}
+
+bool lut_dims_ok(int32_t nb, int32_t ns) {
+    return nb >= 1 && nb <= SLOSIM_MAX_BSZ_BUCKETS && ns >= 1 && ns <= SLOSIM_MAX_SEQ_BUCKETS;
+}
+
+}  // namespace
+
+#define H2D(dst, src, n) CK(cudaMemcpy(dst, src, (n) * sizeof(*(src)), cudaMemcpyHostToDevice))
+#define D2H(dst, src, n) CK(cudaMemcpy(dst, src, (n) * sizeof(*(dst)), cudaMemcpyDeviceToHost))
+
+extern "C" int slosim_lut_lookup(int32_t nb, const int32_t* bb, int32_t ns, const int32_t* sb, const double* sums,
+                                 const int32_t* counts, int64_t n, const int64_t* bsz, const int64_t* seq,
+                                 double* out) {
+    if (!lut_dims_ok(nb, ns) || n < 0) return SLOSIM_EINVAL;
+    bool any = false;
+    for (int c = 0; c < nb * ns; c++) any |= counts[c] > 0;
+    if (!any) return SLOSIM_ECONFIG;
+    for (int64_t k = 0; k < n; k++) if (bsz[k] < 1 || seq[k] < 1) return SLOSIM_EINVAL;
+    if (n == 0) return SLOSIM_OK;
+    std::lock_guard<std::mutex> lock(g_mu);
+    std::vector<double> fs;
+    std::vector<int32_t> fc;
+    frame(nb, ns, sums, counts, fs, fc);
+    CK(snap_reserve(sizeof(ProfTab) + fs.size() * 12 + (size_t)n * 24 + 4096));
+    Bump bp{(char*)g_snap.ptr};
+    ProfTab* tab = bp.take<ProfTab>(1);
+    double* dfs = bp.take<double>(fs.size());
+    int32_t* dfc = bp.take<int32_t>(fc.size());
+    int64_t* db = bp.take<int64_t>(n);
+    int64_t* dsq = bp.take<int64_t>(n);
+    double* dout = bp.take<double>(n);
+    H2D(dfs, fs.data(), fs.size()); H2D(dfc, fc.data(), fc.size()); H2D(db, bsz, n); H2D(dsq, seq, n);
+    k_lut_lookup<<<1, 256>>>(make_snaplut(nb, bb, ns, sb), dfs, dfc, tab, n, db, dsq, dout);
+    CK(cudaGetLastError());
+    D2H(out, dout, n);
+    return SLOSIM_OK;
+}
+
+extern "C" int slosim_decode_formula(int32_t n_base, const int64_t* bx, const double* by, double gamma, int64_t n,
+                                     const int64_t* bsz, const int64_t* seq, double* out) {
+    if (n_base < 1 || n_base > SLOSIM_MAX_BASE_POINTS || n < 0) return SLOSIM_EINVAL;
+    if (n == 0) return SLOSIM_OK;
+    std::lock_guard<std::mutex> lock(g_mu);
+    CK(snap_reserve((size_t)n * 24 + 4096));
+    Bump bp{(char*)g_snap.ptr};
+    int64_t* dbx = bp.take<int64_t>(n_base);
+    double* dby = bp.take<double>(n_base);
+    int64_t* db = bp.take<int64_t>(n);
+    int64_t* dsq = bp.take<int64_t>(n);
+    double* dout = bp.take<double>(n);
+    H2D(dbx, bx, n_base); H2D(dby, by, n_base); H2D(db, bsz, n); H2D(dsq, seq, n);
+    k_formula<<<(unsigned)((n + 255) / 256), 256>>>(n_base, dbx, dby, gamma, n, db, dsq, dout);
+    CK(cudaGetLastError());
+    D2H(out, dout, n);
+    return SLOSIM_OK;
+}
+
+extern "C" int slosim_estimate_duration(int64_t total_tokens, int64_t total_busy_us, int64_t n,
+                                        const int64_t* tokens, int64_t* out) {
+    if (total_busy_us <= 0 || total_tokens <= 0) return SLOSIM_ECONFIG;
+    for (int64_t k = 0; k < n; k++) if (tokens[k] < 0) return SLOSIM_EINVAL;
+    if (n == 0) return SLOSIM_OK;
+    std::lock_guard<std::mutex> lock(g_mu);
+    CK(snap_reserve((size_t)n * 16 + 4096));
+    Bump bp{(char*)g_snap.ptr};
+    int64_t* dt = bp.take<int64_t>(n);
+    int64_t* dout = bp.take<int64_t>(n);
+    H2D(dt, tokens, n);
+    k_estimate<<<(unsigned)((n + 255) / 256), 256>>>(total_tokens, total_busy_us, n, dt, dout);
+    CK(cudaGetLastError());
+    D2H(out, dout, n);
+    return SLOSIM_OK;
+}
+
+extern "C" int slosim_predict_finish(int32_t n, const int64_t* arrival, const int64_t* remaining, int64_t t_now,
+                                     int64_t est_tokens, int64_t est_busy, int64_t* out_finish) {
+    if (n < 0) return SLOSIM_EINVAL;
+    if (est_busy <= 0 || est_tokens <= 0) return SLOSIM_ECONFIG;
+    if (n == 0) return SLOSIM_OK;
+    std::lock_guard<std::mutex> lock(g_mu);
+    CK(snap_reserve((size_t)n * 24 + 4096));
+    Bump bp{(char*)g_snap.ptr};
+    int64_t* da = bp.take<int64_t>(n);
+    int64_t* dr = bp.take<int64_t>(n);
+    int64_t* dout = bp.take<int64_t>(n);
+    H2D(da, arrival, n); H2D(dr, remaining, n);
+    k_predict<<<1, 32>>>(n, da, dr, t_now, est_tokens, est_busy, dout);
+    CK(cudaGetLastError());
+    D2H(out_finish, dout, n);
+    return SLOSIM_OK;
+}
+
+extern "C" int slosim_select_prefill(int32_t policy, int32_t n, const int64_t* arrival, const int32_t* input_len,
+                                     const int64_t* remaining, const int32_t* id_rank, int64_t budget, int64_t t_now,
+                                     int64_t est_tokens, int64_t est_busy, int64_t ttft_slo_us, int32_t* out_index,
+                                     int64_t* out_take, int32_t* n_out, double* out_scores) {
+    if (budget < 1 || n < 0 || policy < 0 || policy > 2) return SLOSIM_EINVAL;
+    if (policy == SLOSIM_PREFILL_KAIROS_URGENCY && n > 0 && (est_busy <= 0 || est_tokens <= 0)) return SLOSIM_ECONFIG;
+    if (n == 0) { *n_out = 0; return SLOSIM_OK; }
+    std::lock_guard<std::mutex> lock(g_mu);
+    size_t wsb = ws_bytes(n);
+    CK(snap_reserve(wsb + (size_t)n * 64 + 8192));
+    Bump bp{(char*)g_snap.ptr};
+    char* dws = bp.take<char>(wsb);
+    int64_t* da = bp.take<int64_t>(n);
+    int32_t* di = bp.take<int32_t>(n);
+    int64_t* dr = bp.take<int64_t>(n);
+    int32_t* dk = bp.take<int32_t>(n);
+    int32_t* doi = bp.take<int32_t>(n);
+    int64_t* dot = bp.take<int64_t>(n);
+    int32_t* dno = bp.take<int32_t>(1);
+    double* dsc = bp.take<double>(n);
+    H2D(da, arrival, n); H2D(di, input_len, n); H2D(dr, remaining, n); H2D(dk, id_rank, n);
+    k_select_prefill<<<1, 32>>>(policy, n, da, di, dr, dk, budget, t_now, est_tokens, est_busy, ttft_slo_us, dws, n,
+                                doi, dot, dno, dsc);
+    CK(cudaGetLastError());
+    D2H(n_out, dno, 1);
+    D2H(out_index, doi, *n_out);
+    D2H(out_take, dot, *n_out);
+    if (out_scores && policy == SLOSIM_PREFILL_KAIROS_URGENCY) D2H(out_scores, dsc, n);
+    return SLOSIM_OK;
+}
+
+extern "C" int slosim_select_decode(int32_t policy, int32_t n, const int64_t* seq_len, const int32_t* id_rank,
+                                    const int64_t* n_gen, const double* t_first, double t_now, int64_t tpot_slo_us,
+                                    int32_t nb, const int32_t* bb, int32_t ns, const int32_t* sb, const double* sums,
+                                    const int32_t* counts, int32_t* out_batch, int32_t* n_batch, int32_t* out_delayed,
+                                    int32_t* n_delayed, double* out_admit_times, double* out_pred, double* out_smin,
+                                    int32_t* out_fallback) {
+    if (n < 1 || policy < 0 || policy > 1 || !lut_dims_ok(nb, ns)) return SLOSIM_EINVAL;
+    bool any = false;
+    for (int c = 0; c < nb * ns; c++) any |= counts[c] > 0;
+    if (!any) return SLOSIM_ECONFIG;
+    std::lock_guard<std::mutex> lock(g_mu);
+    std::vector<double> fs;
+    std::vector<int32_t> fc;
+    frame(nb, ns, sums, counts, fs, fc);
+    size_t wsb = ws_bytes(n);
+    CK(snap_reserve(wsb + sizeof(ProfTab) + fs.size() * 12 + (size_t)n * 64 + 8192));
+    Bump bp{(char*)g_snap.ptr};
+    char* dws = bp.take<char>(wsb);
+    ProfTab* tab = bp.take<ProfTab>(1);
+    double* dfs = bp.take<double>(fs.size());
+    int32_t* dfc = bp.take<int32_t>(fc.size());
+    int64_t* dseq = bp.take<int64_t>(n);
+    int32_t* didr = bp.take<int32_t>(n);
+    int64_t* dng = bp.take<int64_t>(n);
+    double* dtf = bp.take<double>(n);
+    int32_t* db = bp.take<int32_t>(n);
+    int32_t* dd = bp.take<int32_t>(n);
+    double* dt = bp.take<double>(n);
+    int32_t* dnb = bp.take<int32_t>(4);
+    double* dsc = bp.take<double>(2);
+    H2D(dfs, fs.data(), fs.size()); H2D(dfc, fc.data(), fc.size());
+    H2D(dseq, seq_len, n); H2D(didr, id_rank, n); H2D(dng, n_gen, n); H2D(dtf, t_first, n);
+    k_select_decode<<<1, 32>>>(policy, n, dseq, didr, dng, dtf, t_now, tpot_slo_us, make_snaplut(nb, bb, ns, sb), dfs,
+                               dfc, tab, dws, n, db, dnb, dd, dnb + 1, dt, dsc, dsc + 1, dnb + 2);
+    CK(cudaGetLastError());
+    int32_t hn[4];
+    D2H(hn, dnb, 3);
+    double hs[2];
+    D2H(hs, dsc, 2);
+    *n_batch = hn[0]; *n_delayed = hn[1]; *out_fallback = hn[2]; *out_pred = hs[0]; *out_smin = hs[1];
+    D2H(out_batch, db, hn[0]);
+    if (hn[1]) D2H(out_delayed, dd, hn[1]);
+    if (out_admit_times && !hn[2] && policy == SLOSIM_DECODE_KAIROS_SLACK) D2H(out_admit_times, dt, hn[0]);
+    return SLOSIM_OK;
+}
+
+extern "C" int slosim_prefill_batch_us(int32_t n_curve, const int64_t* cx, const int64_t* cy, int32_t k,
+                                       const int64_t* done_before, const int64_t* take, int64_t* out_us) {
+    if (n_curve < 2 || n_curve > SLOSIM_MAX_CURVE_POINTS || k < 0) return SLOSIM_EINVAL;
+    std::lock_guard<std::mutex> lock(g_mu);
+    CK(snap_reserve((size_t)(k + 1) * 16 + 8192));
+    Bump bp{(char*)g_snap.ptr};
+    int64_t* dx = bp.take<int64_t>(n_curve);
+    int64_t* dy = bp.take<int64_t>(n_curve);
+    int64_t* dd = bp.take<int64_t>(k + 1);
+    int64_t* dt = bp.take<int64_t>(k + 1);
+    int64_t* dout = bp.take<int64_t>(1);
+    H2D(dx, cx, n_curve); H2D(dy, cy, n_curve);
+    if (k) { H2D(dd, done_before, k); H2D(dt, take, k); }
+    k_prefill_gt<<<1, 32>>>(n_curve, dx, dy, k, dd, dt, dout);
+    CK(cudaGetLastError());
+    D2H(out_us, dout, 1);
+    return SLOSIM_OK;
+}
+
+extern "C" int slosim_request_metrics(int64_t n, const int64_t* arrival, const int64_t* output_len,
+                                      const int64_t* ts_offsets, const int64_t* ts, int64_t ttft_slo_us,
+                                      int64_t tpot_slo_us, int64_t* ttft_us, double* mean_tpot, double* tps,
+                                      uint8_t* met_flags, int32_t* misses, double* agg) {
+    if (n < 0) return SLOSIM_EINVAL;
+    if (n == 0) {
+        if (agg) { agg[0] = agg[1] = agg[2] = 1.0; agg[3] = agg[4] = NAN; }
+        return SLOSIM_OK;
+    }
+    int64_t nts = ts_offsets[n];
+    for (int64_t k = 0; k < n; k++) if (ts_offsets[k + 1] - ts_offsets[k] < 1) return SLOSIM_EINVAL;
+    std::lock_guard<std::mutex> lock(g_mu);
+    CK(snap_reserve((size_t)n * 80 + (size_t)nts * 8 + 8192));
+    Bump bp{(char*)g_snap.ptr};
+    int64_t* da = bp.take<int64_t>(n);
+    int64_t* dol = bp.take<int64_t>(n);
+    int64_t* doff = bp.take<int64_t>(n + 1);
+    int64_t* dts = bp.take<int64_t>(nts);
+    int64_t* dtt = bp.take<int64_t>(n);
+    double* dtp = bp.take<double>(n);
+    double* dtr = bp.take<double>(n);
+    uint8_t* dfl = bp.take<uint8_t>(n);
+    int32_t* dmi = bp.take<int32_t>(n);
+    double* dscr = bp.take<double>(n);
+    double* dagg = bp.take<double>(5);
+    H2D(da, arrival, n); H2D(dol, output_len, n); H2D(doff, ts_offsets, n + 1); H2D(dts, ts, nts);
+    k_request_metrics<<<(unsigned)((n + 127) / 128), 128>>>(n, da, dol, doff, dts, ttft_slo_us, tpot_slo_us, dtt, dtp,
+                                                            dtr, dfl, dmi);
+    CK(cudaGetLastError());
+    k_aggregate<<<1, 32>>>(n, dfl, dtr, dscr, dagg);
+    CK(cudaGetLastError());
+    if (ttft_us) D2H(ttft_us, dtt, n);
+    if (mean_tpot) D2H(mean_tpot, dtp, n);
+    if (tps) D2H(tps, dtr, n);
+    if (met_flags) D2H(met_flags, dfl, n);
+    if (misses) D2H(misses, dmi, n);
+    if (agg) D2H(agg, dagg, 5);
+    return SLOSIM_OK;
+}
+
+extern "C" int slosim_synth_profile(slosim_profile_t* profile, int32_t n_anchors, const int64_t* anchor_bsz,
+                                    const int64_t* anchor_seq, const double* anchor_us, double batch_growth,
+                                    int64_t prior_weight) {
+    if (!profile || !lut_dims_ok(profile->nb, profile->ns) || n_anchors < 1 || batch_growth < 0 || prior_weight < 0)
+        return SLOSIM_EINVAL;
+    int nbase = 0;
+    for (int k = 0; k < n_anchors; k++) nbase += anchor_bsz[k] == 1;
+    if (nbase == 0 || nbase > SLOSIM_MAX_BASE_POINTS) return SLOSIM_EINVAL;
+    std::lock_guard<std::mutex> lock(g_mu);
+    CK(snap_reserve(sizeof(slosim_profile_t) + (size_t)n_anchors * 24 + 8192));
+    Bump bp{(char*)g_snap.ptr};
+    slosim_profile_t* dp = bp.take<slosim_profile_t>(1);
+    int64_t* dab = bp.take<int64_t>(n_anchors);
+    int64_t* das = bp.take<int64_t>(n_anchors);
+    double* dau = bp.take<double>(n_anchors);
+    H2D(dp, profile, 1); H2D(dab, anchor_bsz, n_anchors); H2D(das, anchor_seq, n_anchors);
+    H2D(dau, anchor_us, n_anchors);
+    k_synth<<<1, 256>>>(dp, n_anchors, dab, das, dau, batch_growth, prior_weight);
+    CK(cudaGetLastError());
+    D2H(profile, dp, 1);
+    return SLOSIM_OK;
+}
+
+extern "C" int slosim_abi_version(void) { return SLOSIM_ABI_VERSION; }
+
+extern "C" int slosim_device_count(void) {
+    int n = 0;
+    if (cudaGetDeviceCount(&n) != cudaSuccess) return 0;
+    return n;
+}
+
+extern "C" const char* slosim_build_info(void) {
+    return "slosim_b200 abi=" "1" " arch=sm_100a fmad=false";
+}
+
+extern "C" const char* slosim_last_error(void) { return g_err; }

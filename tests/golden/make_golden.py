@@ -1,0 +1,243 @@
+"""Generate golden fixtures by running the REFERENCE slosim package (Python).
+
+Run in the build container (where /root/reference exists):
+
+    python tests/golden/make_golden.py
+
+It imports /root/reference/pkg/src/slosim unmodified and records, for a set of
+workloads x configs, the per-instance summary (met counts, p50/p90, worst wait,
+step counts, byte-model counters), per-request rows, and the decision digest
+computed from the reference's own event log with the digest definition shared
+by the CUDA engine and the C oracle.  The
+fixtures are committed; the GPU box never needs /root/reference.
+"""
+
+from __future__ import annotations
+
+import gzip
+import hashlib
+import json
+import math
+import os
+import random
+import sys
+
+REF = "/root/reference/pkg/src"
+HERE = os.path.dirname(os.path.abspath(__file__))
+M64 = (1 << 64) - 1
+
+
+def mix64(x):
+    x &= M64
+    x ^= x >> 30
+    x = (x * 0xBF58476D1CE4E5B9) & M64
+    x ^= x >> 27
+    x = (x * 0x94D049BB133111EB) & M64
+    x ^= x >> 31
+    return x
+
+
+def digest_from_events(events, pos_of):
+    """Decision digest over the reference event log (PrefillStepDone/DecodeStepDone)."""
+    D = 0
+    for ev in events:
+        if ev["kind"] == "PrefillStepDone":
+            h = mix64(ev["t_us"] ^ 0xA5A5A5A5A5A5A5A5)
+            for rid, take in ev["detail"]["batch"]:
+                h = mix64(h ^ ((pos_of[rid] << 32) | take))
+            h = mix64(h ^ ev["detail"]["duration_us"])
+            D = mix64(D ^ h)
+        elif ev["kind"] == "DecodeStepDone":
+            s = 0
+            for rid in ev["detail"]["batch"]:
+                s = (s + mix64(pos_of[rid] + 0x9E3779B97F4A7C15)) & M64
+            h = mix64(ev["t_us"] ^ 0x5A5A5A5A5A5A5A5A)
+            h = mix64(h ^ s)
+            h = mix64(h ^ ev["detail"]["bsz"])
+            h = mix64(h ^ ev["detail"]["duration_us"])
+            D = mix64(D ^ h)
+    return D
+
+
+def appendix_c_digest(events):
+    """SURVEY Appendix C digest: SHA-256 over json.dumps of the step records."""
+    h = hashlib.sha256()
+    for ev in events:
+        if ev["kind"] == "DecodeStepDone":
+            h.update(json.dumps([ev["t_us"], sorted(ev["detail"]["batch"]), ev["detail"]["duration_us"]]).encode())
+        elif ev["kind"] == "PrefillStepDone":
+            h.update(json.dumps([ev["t_us"], ev["detail"]["batch"], ev["detail"]["duration_us"]]).encode())
+    return h.hexdigest()[:16]
+
+
+def byte_counters(slosim, sim_cls, cfg, workload):
+    """V_dec, B_dec, V_pre by wrapping the reference registries."""
+    from slosim import engine as E
+
+    c = {"v_dec": 0, "b_dec": 0, "v_pre": 0, "max_queue": 0, "max_active": 0}
+    pp = E.PREFILL_POLICIES[cfg.prefill_policy]
+    dp = E.DECODE_POLICIES[cfg.decode_policy]
+
+    def pw(queue, budget, t, est, slo):
+        c["v_pre"] += len(queue)
+        c["max_queue"] = max(c["max_queue"], len(queue))
+        return pp(queue, budget, t, est, slo)
+
+    def dw(active, t, slo, lut):
+        c["v_dec"] += len(active)
+        c["max_active"] = max(c["max_active"], len(active))
+        sel = dp(active, t, slo, lut)
+        c["b_dec"] += len(sel.batch)
+        return sel
+
+    sim = sim_cls(cfg, workload, collect_events=True)
+    sim._prefill_policy = pw
+    sim._decode_policy = dw
+    return sim, c
+
+
+def run_reference(slosim, cfg, workload):
+    """Run one reference simulation; return a summary dict + per-request rows."""
+    from slosim.engine import Simulation
+
+    order = sorted(range(len(workload)), key=lambda k: (workload[k].arrival_time, workload[k].id))
+    pos_of = {workload[k].id: p for p, k in enumerate(order)}
+    try:
+        sim, cnt = byte_counters(slosim, Simulation, cfg, workload)
+    except slosim.ConfigurationError:
+        return {"status": 3}
+    try:
+        rep = sim.run()
+    except slosim.ConfigurationError:
+        return {"status": 3}
+    ev = sim.events
+    tps = [r.decode_tps for r in rep.rows if r.decode_tps is not None]
+    rows = {}
+    for r in sim.requests:
+        m = next(x for x in rep.rows if x.id == r.id)
+        rows[pos_of[r.id]] = {
+            "ttft_us": m.ttft_us, "mean_tpot_us": m.mean_tpot_us, "decode_tps": m.decode_tps,
+            "flags": int(m.ttft_met) | (int(m.tpot_met) << 1) | (int(m.e2e_met) << 2),
+            "deadline_misses": m.deadline_misses, "t_prefill_finish": r.t_prefill_finish,
+            "t_first_token": r.t_first_token, "t_last_token": r.token_timestamps[-1] if r.token_timestamps else None,
+            "first_sched_us": sim._first_sched.get(r.id),
+        }
+    return {
+        "status": 0,
+        "n": len(workload),
+        "ttft_met": sum(x.ttft_met for x in rep.rows),
+        "tpot_met": sum(x.tpot_met for x in rep.rows),
+        "e2e_met": sum(x.e2e_met for x in rep.rows),
+        "n_tps": len(tps),
+        "tps_p50": rep.decode_tps_p50,
+        "tps_p90": rep.decode_tps_p90,
+        "worst_queue_wait_us": rep.worst_queue_wait_us,
+        "prefill_steps": sum(1 for e in ev if e["kind"] == "PrefillStepDone"),
+        "decode_steps": sum(1 for e in ev if e["kind"] == "DecodeStepDone"),
+        "digest": str(digest_from_events(ev, pos_of)),
+        "digest_c": appendix_c_digest(ev),
+        "v_dec": cnt["v_dec"], "b_dec": cnt["b_dec"], "v_pre": cnt["v_pre"],
+        "max_queue": cnt["max_queue"], "max_active": cnt["max_active"],
+        "deadline_misses": sum(x.deadline_misses for x in rep.rows),
+        "est_tokens": sim.estimator.total_tokens, "est_busy_us": sim.estimator.total_busy_us,
+        "ttft_att": rep.ttft_attainment, "tpot_att": rep.tpot_attainment, "e2e_att": rep.e2e_attainment,
+        "rows": rows,
+    }
+
+
+def wl_to_json(workload):
+    return [[r.id, r.arrival_time, r.input_len, r.output_len, r.prefix_hit_len] for r in workload]
+
+
+def cfg_to_json(cfg):
+    p = cfg.profile
+    return {
+        "chunk_budget": cfg.chunk_budget, "kv_capacity_tokens": cfg.kv_capacity_tokens,
+        "transfer_base_us": cfg.transfer_base_us, "transfer_per_token_us": cfg.transfer_per_token_us,
+        "prefill_policy": cfg.prefill_policy, "decode_policy": cfg.decode_policy,
+        "ttft_slo_us": cfg.slo.ttft_slo_us, "tpot_slo_us": cfg.slo.tpot_slo_us, "seed": cfg.seed,
+        "profile": {
+            "decode_anchors": [list(a) for a in p.decode_anchors], "batch_growth": p.batch_growth,
+            "prior_weight": p.prior_weight, "bsz_buckets": p.bsz_buckets, "seq_buckets": p.seq_buckets,
+            "prefill_anchor": list(p.prefill_anchor),
+            "prefill_gt_curve": [list(x) for x in p.prefill_gt_curve] if p.prefill_gt_curve else None,
+            "decode_noise_eps": p.decode_noise_eps,
+        },
+    }
+
+
+def random_case(slosim, rng, k):
+    """Random small workload + config covering every policy pair and knob."""
+    n = rng.randrange(1, 41)
+    wl = []
+    for i in range(n):
+        inp = rng.choice([rng.randrange(1, 3000), rng.randrange(1, 20000), rng.randrange(60000, 140000)])
+        hit = rng.randrange(0, inp) if rng.random() < 0.2 else 0
+        wl.append(slosim.Request(id=f"q{rng.randrange(10**6):06d}_{i}", arrival_time=rng.randrange(0, 4_000_000),
+                                 input_len=inp, output_len=rng.choice([1, rng.randrange(1, 60), rng.randrange(1, 300)]),
+                                 prefix_hit_len=hit))
+    if rng.random() < 0.2:  # equal arrivals with ids out of position order
+        for r in wl[: n // 2]:
+            r.arrival_time = 1_000_000
+    wl.sort(key=lambda r: r.arrival_time)  # engine only requires arrival order
+    pp = ["fcfs", "sjf", "kairos-urgency"][k % 3]
+    dp = ["continuous", "kairos-slack"][(k // 3) % 2]
+    worst = max(r.input_len + r.output_len for r in wl)
+    kv = worst + rng.choice([0, rng.randrange(0, 50_000), 2_000_000])
+    anchors = rng.choice([
+        [(1, 8192, 11_000), (1, 131072, 40_300)],
+        [(1, 1024, 9_000), (1, 65536, 42_000)],
+        [(1, 4096, 7_000), (1, 32768, 15_000), (1, 131072, 60_000), (4, 8192, 30_000)],
+    ])
+    bsz_b = rng.choice([None, None, [1, 3, 8, 20], [2, 4, 16, 64, 256]])
+    seq_b = rng.choice([None, None, [1000, 10000, 100000, 200000], [8192 * k for k in range(1, 9)]])
+    curve = rng.choice([None, None, [(8192, 400_400), (131072, 8_800_000)], [(5000, 300_000), (50000, 4_000_000)]])
+    eps = rng.choice([0.0, 0.0, 0.0, 0.25])
+    prof = slosim.CostProfile(decode_anchors=anchors, batch_growth=rng.choice([0.0, 0.03, 0.05]),
+                              prior_weight=rng.choice([100, 100, 1, 7]), bsz_buckets=bsz_b, seq_buckets=seq_b,
+                              prefill_anchor=rng.choice([(131072, 8_800_000), (10_000, 1_000_000), (139264, 9_200_400)]),
+                              prefill_gt_curve=curve, decode_noise_eps=eps)
+    cfg = slosim.ClusterConfig(
+        chunk_budget=rng.choice([512, 2000, 4096, 8192, 8192]), kv_capacity_tokens=kv,
+        transfer_base_us=rng.choice([0, 0, 150]), transfer_per_token_us=rng.choice([0.0, 0.0, 0.25, 1.0]),
+        prefill_policy=pp, decode_policy=dp,
+        slo=slosim.SLOConfig(ttft_slo_us=rng.choice([8_000_000, 2_000_000, 500_000]),
+                             tpot_slo_us=rng.choice([50_000, 20_000, 100_000])),
+        profile=prof, seed=rng.randrange(1000))
+    return wl, cfg
+
+
+def main():
+    sys.path.insert(0, REF)
+    import slosim
+
+    out = {"meta": {"reference": "slosim @ /root/reference/pkg/src", "numpy": __import__("numpy").__version__}}
+    # --- config 1: 6 rates x 2 pairs on gen_longtail(LongTailSpec())
+    base = slosim.gen_longtail(slosim.LongTailSpec())
+    c1 = []
+    for qps in [0.4, 0.7, 1.0, 1.3, 1.6, 1.9]:
+        wl = slosim.rescale_qps(base, qps)
+        for pp, dp in [("fcfs", "continuous"), ("kairos-urgency", "kairos-slack")]:
+            cfg = slosim.ClusterConfig(prefill_policy=pp, decode_policy=dp)
+            s = run_reference(slosim, cfg, wl)
+            s.pop("rows")
+            c1.append({"qps": qps, "pair": f"{pp}+{dp}", "summary": s})
+            print("config1", qps, pp, s["e2e_met"], s["digest_c"], flush=True)
+    out["config1"] = c1
+    # --- random engine cases (all policy pairs, every knob)
+    rng = random.Random(20260101)
+    cases = []
+    for k in range(int(os.environ.get("GOLDEN_CASES", "240"))):
+        wl, cfg = random_case(slosim, rng, k)
+        s = run_reference(slosim, cfg, wl)
+        cases.append({"workload": wl_to_json(wl), "config": cfg_to_json(cfg), "summary": s})
+    out["cases"] = cases
+    print("cases", len(cases), sum(1 for c in cases if c["summary"]["status"] == 3), "config errors")
+    path = os.path.join(HERE, "engine_golden.json.gz")
+    with gzip.open(path, "wt", encoding="utf-8") as f:
+        json.dump(out, f, sort_keys=True)
+    print("wrote", path, os.path.getsize(path))
+
+
+if __name__ == "__main__":
+    main()
