@@ -1,0 +1,393 @@
+"""Benchmark: simulated requests/sec of the batched Kairos simulator on 1..8 B200.
+
+Workload (BASELINE.json metric "simulated requests/sec (1/2/4/8 B200)"): SURVEY
+Appendix B config 5 — 256 trace seeds x 64 arrival rates x 16 SLO scales x 4
+policy pairs = 1,048,576 independent instances of 1k requests, sharded across
+GPUs.  One *step* is one slice of 16,384 instances (16.4M simulated requests)
+per GPU; rank r takes slices s*G + r (weak scaling).  The timed region is K
+steps (kernel launches on device-resident inputs, L2 flushed between steps by
+a 256 MiB write) followed by the final exchange: the per-(pair, rate, SLO)
+e2e-attainment histogram build, an NCCL int64 all-reduce and an all-gather of
+the summary rows.
+
+JSON line keys follow the driver contract; `e2e` re-measures the same metric
+through the C-ABI host-buffer entry point (slosim_run_batch_host) with pinned
+host inputs and every H2D/D2H copy inside the timed region; `roofline` uses
+the SURVEY §8(d) algorithmic byte model; `cpu_baseline` times the C oracle
+port (all host threads) on a bounded sample of the same slice and checks the
+GPU results against it bit-for-bit.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl reference] [--workload config5|config3|config2]
+"""
+
+from __future__ import annotations
+
+import argparse
+import ctypes
+import json
+import os
+import subprocess
+import sys
+import tempfile
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+SLICE = 16384
+N_CONFIG5 = 256 * 64 * 16 * 4
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--workload", default="config5", choices=["config5", "config3", "config2"])
+    ap.add_argument("--slice", type=int, default=SLICE)
+    ap.add_argument("--cpu-sample-s", type=float, default=12.0, help="target seconds of oracle work")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true")
+    return ap.parse_args()
+
+
+def dist_env():
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return world, rank, local
+
+
+def metric_name():
+    return "simulated requests/sec (1/2/4/8 B200) at oracle-exact SLO attainment vs CPU ref"
+
+
+def alg_bytes(summ: np.ndarray) -> int:
+    """B = 24N + 16 V_dec + 12 B_dec + 20 V_pre + 8 N_tps + 96 per instance."""
+    return int(24 * summ["n"].astype(np.int64).sum() + 16 * summ["v_dec"].sum() + 12 * summ["b_dec"].sum()
+               + 20 * summ["v_pre"].sum() + 8 * summ["n_tps"].astype(np.int64).sum() + 96 * len(summ))
+
+
+def load_peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            p = json.load(f)
+        return float(p["hbm_gbs"]), "measured"
+    except Exception:
+        return 6650.0, "fallback"
+
+
+def profile_traffic():
+    """dram bytes per launch of the dominant kernel from the committed ncu summary, if any."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "ncu_summary.json")) as f:
+            d = json.load(f)
+        return d.get("dram_bytes_per_launch"), d.get("alg_bytes_per_launch")
+    except Exception:
+        return None, None
+
+
+class ClockSampler:
+    def __init__(self, device_index=0):
+        self.fd, self.path = tempfile.mkstemp(suffix=".csv")
+        os.close(self.fd)
+        q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+             "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+             "clocks_event_reasons.sw_power_cap")
+        try:
+            self.p = subprocess.Popen(["nvidia-smi", "-i", str(device_index), f"--query-gpu={q}",
+                                       "--format=csv,noheader,nounits", "-lms", "200"],
+                                      stdout=open(self.path, "w"), stderr=subprocess.DEVNULL)
+        except Exception:
+            self.p = None
+
+    def stop(self):
+        if self.p is None:
+            return None
+        self.p.terminate()
+        try:
+            self.p.wait(timeout=5)
+        except Exception:
+            self.p.kill()
+        sm, mx, reasons = [], 0.0, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        with open(self.path) as f:
+            for line in f:
+                parts = [x.strip() for x in line.split(",")]
+                if len(parts) < 7:
+                    continue
+                try:
+                    sm.append(float(parts[0]))
+                    mx = max(mx, float(parts[1]))
+                except ValueError:
+                    continue
+                for nm, v in zip(names, parts[3:7]):
+                    if v.lower().startswith("active"):
+                        reasons.add(nm)
+        os.unlink(self.path)
+        if not sm:
+            return None
+        load = [x for x in sm if x > 0.5 * mx] or sm
+        return {"sm_mhz": float(np.median(load)), "sm_max_mhz": mx, "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+# ------------------------------------------------------------- workloads ---
+def build_workload(name, synth=None, select=None):
+    from paper_2605_02329_b200 import batch as B
+
+    if name == "config5":
+        return B.config5(select=select, synth=synth)
+    if name == "config3":
+        return B.config3(select=select, synth=synth)
+    return B.config2(select=select, synth=synth)
+
+
+def workload_meta(name, slice_n):
+    if name == "config5":
+        return {"workload": "config5: 256 seeds x 64 rates x 16 SLO scales x 4 policy pairs, 1k-request long-tail "
+                            "traces (1,048,576 instances)", "instances_per_step_per_gpu": slice_n,
+                "requests_per_instance": 1000, "policy_pairs": ["fcfs+continuous", "fcfs+kairos-slack",
+                                                                "kairos-urgency+continuous",
+                                                                "kairos-urgency+kairos-slack"],
+                "l2": "flushed between steps (256 MiB write)"}
+    if name == "config3":
+        return {"workload": "config3: 64 rates x 16 SLO scales x 3 policy pairs on the config-1 trace (3072 instances)",
+                "l2": "flushed between steps (256 MiB write)"}
+    return {"workload": "config2: one 100k-request long-tail trace, kairos and fcfs pairs (2 instances)",
+            "l2": "flushed between steps (256 MiB write)"}
+
+
+# ---------------------------------------------------------- reference arm --
+def run_reference(args):
+    world, rank, _ = dist_env()
+    if rank != 0:
+        return 0
+    from oracle import oracle
+
+    threads = os.cpu_count() or 1
+    n_total = N_CONFIG5 if args.workload == "config5" else (3072 if args.workload == "config3" else 2)
+    # per step: a bounded stride sample of the step's slice (~cpu_sample_s / steps seconds each)
+    per_step = {"config5": 1536, "config3": 768, "config2": 2}[args.workload]
+    times, reqs = [], []
+    for s in range(args.warmup + args.steps):
+        start = (s * args.slice) % n_total
+        sel = (start + np.sort(np.random.default_rng(s).choice(args.slice, per_step, replace=False))) % n_total
+        if args.workload == "config2":
+            sel = np.arange(2)
+        sw = build_workload(args.workload, synth=oracle.synth, select=sel)
+        t0 = time.perf_counter()
+        oracle.run_batch(sw.packed, threads=threads)
+        dt = time.perf_counter() - t0
+        if s >= args.warmup:
+            times.append(dt)
+            reqs.append(sw.packed.n_requests)
+    T = sum(times)
+    value = sum(reqs) / T
+    line = {
+        "impl": "reference", "metric": metric_name(), "value": value, "unit": "simulated requests/s",
+        "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * T / args.steps,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "int64+f64",
+        "data": "synthetic (reference LongTailSpec generator, host numpy)",
+        "config": dict(workload_meta(args.workload, args.slice), sample=f"{per_step} instances per step (seeded random sample of the step slice)"),
+        "cpu_baseline": {"value": value, "unit": "simulated requests/s", "cores": threads, "kind": "port",
+                         "sample": f"{per_step} random instances/step x {args.steps} steps of {args.workload}, C oracle "
+                                   f"(oracle/slosim_oracle.c), {threads} threads"},
+        "e2e": {"value": value, "unit": "simulated requests/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+# ----------------------------------------------------------------- ours ---
+def main():
+    args = parse()
+    if args.impl == "reference":
+        return run_reference(args)
+    import torch
+    import torch.distributed as dist
+
+    from paper_2605_02329_b200 import _abi
+    from paper_2605_02329_b200 import dist as D
+    from paper_2605_02329_b200.batch import DeviceBatch
+
+    world, rank, local = dist_env()
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    L = _abi.lib()
+
+    # full instance grid resident in HBM (instances + traces), summaries per instance
+    n_total = N_CONFIG5 if args.workload == "config5" else (3072 if args.workload == "config3" else 2)
+    slice_n = min(args.slice, n_total) if args.workload != "config2" else 2
+    n_slices = max(1, n_total // slice_n)
+    sw = build_workload(args.workload)
+    db = DeviceBatch(sw.packed)
+    pk = sw.packed
+    n_pairs, n_slo, n_rates = {"config5": (4, 16, 64), "config3": (3, 16, 64), "config2": (2, 1, 1)}[args.workload]
+    n_cells = n_pairs * n_slo * n_rates
+    cells = torch.from_numpy(D.cell_ids_config_grid(np.arange(n_total), n_pairs, n_slo, n_rates)).cuda()
+    hist = torch.zeros(n_cells * 1001, dtype=torch.int64, device="cuda")
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
+    stream = torch.cuda.current_stream()
+
+    def step(slice_id):
+        db.launch_range(slice_id * slice_n, slice_n)
+
+    for s in D.slices_for_rank(n_slices, world, rank, args.warmup, 0):
+        flush.fill_(1)
+        step(s)
+    torch.cuda.synchronize()
+    timed = D.slices_for_rank(n_slices, world, rank, args.steps, args.warmup)
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in timed]
+    clk = ClockSampler(local)
+    time.sleep(0.3)
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    t_start = torch.cuda.Event(enable_timing=True)
+    t_end = torch.cuda.Event(enable_timing=True)
+    t_start.record()
+    for (e0, e1), s in zip(ev, timed):
+        flush.fill_(1)
+        e0.record()
+        step(s)
+        e1.record()
+    # final exchange: histogram of this rank's instances, int64 all-reduce, summary all-gather
+    hist.zero_()
+    for s in timed:
+        off = s * slice_n
+        L.slosim_histogram(slice_n, ctypes.c_void_p(db.summaries.data_ptr() + off * 136),
+                           ctypes.c_void_p(cells.data_ptr() + off * 4), 1001, ctypes.c_void_p(hist.data_ptr()),
+                           ctypes.c_void_p(stream.cuda_stream))
+    mine = torch.cat([db.summaries[s * slice_n * 136:(s + 1) * slice_n * 136] for s in timed])
+    gathered, hist = D.exchange(mine, hist)
+    t_end.record()
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    clocks = clk.stop()
+    elapsed_ms = t_start.elapsed_time(t_end)
+    step_ms = [e0.elapsed_time(e1) for e0, e1 in ev]
+    tmax = torch.tensor([elapsed_ms], dtype=torch.float64, device="cuda")
+    if world > 1:
+        dist.all_reduce(tmax, op=dist.ReduceOp.MAX)
+    elapsed_ms = float(tmax.item())
+
+    host = db.summaries.cpu().numpy().view(_abi.summary_dtype())
+    timed_idx = np.concatenate([np.arange(s * slice_n, (s + 1) * slice_n) for s in timed])
+    summ = host[timed_idx]
+    assert np.all(summ["status"] == 0), "engine reported a failed instance"
+    reqs_rank = int(summ["n"].astype(np.int64).sum())
+    reqs_all = reqs_rank * world
+    value = reqs_all / (elapsed_ms / 1e3)
+
+    # roofline of the dominant kernel (sim_kernel): algorithmic bytes / mean launch duration
+    peak, peak_kind = load_peaks()
+    abytes = alg_bytes(summ) / len(timed)
+    mean_ms = float(np.mean(step_ms))
+    achieved = abytes / (mean_ms / 1e3) / 1e9
+    traffic, _ = profile_traffic()
+
+    # e2e through the C-ABI with host buffers (pinned), copies inside the timed region
+    e2e = None
+    if not args.no_e2e:
+        e2e = measure_e2e(args, sw, timed, slice_n, world)
+
+    cpu = None
+    parity = None
+    if rank == 0 and not args.no_cpu:
+        cpu, parity = cpu_baseline(args, host, timed[0], slice_n)
+
+    if rank == 0:
+        line = {
+            "metric": metric_name(), "value": value, "unit": "simulated requests/s", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": elapsed_ms / args.steps,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "int64+f64",
+            "data": "synthetic (reference LongTailSpec generator, host numpy; identical traces on CPU and GPU)",
+            "config": dict(workload_meta(args.workload, slice_n), parallelism=f"instances sharded over {world} GPU(s)"),
+            "e2e": e2e,
+            "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "peak_kind": peak_kind, "unit": "GB/s",
+                         "frac": achieved / peak, "traffic": traffic,
+                         "alg_bytes_per_launch": abytes, "mean_launch_ms": mean_ms},
+            "cpu_baseline": cpu,
+            "parity": parity,
+            "clocks": clocks,
+            "gpu_launches": 2 * len(timed) + len(timed),
+            "kernel_ms_per_step": step_ms,
+        }
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+    return 0
+
+
+def measure_e2e(args, sw, timed, slice_n, world):
+    """Same metric through slosim_run_batch_host: pinned host inputs, H2D + kernels + D2H per step."""
+    import torch
+
+    from paper_2605_02329_b200 import _abi
+    from paper_2605_02329_b200.pack import PackedBatch
+
+    pk = sw.packed
+    pin = lambda a: torch.from_numpy(np.array(a, copy=True)).pin_memory().numpy()
+    arr, inp, out, hit, idr = pin(pk.arrival), pin(pk.inp), pin(pk.out), pin(pk.hit), pin(pk.idr)
+    times, reqs, h2d, d2h = [], 0, 0, 0
+    for s in timed:
+        inst = pin(pk.instances[s * slice_n:(s + 1) * slice_n].view(np.uint8)).view(_abi.instance_dtype())
+        part = PackedBatch(arr, inp, out, hit, idr, pk.profiles, inst, 0, 0, 0)
+        part.summaries = pin(part.summaries.view(np.uint8)).view(_abi.summary_dtype())
+        b = part.host_struct()
+        t0 = time.perf_counter()
+        rc = _abi.lib().slosim_run_batch_host(ctypes.byref(b), None)
+        times.append(time.perf_counter() - t0)
+        assert rc == 0
+        reqs += part.n_requests
+        h2d = arr.nbytes + inp.nbytes + out.nbytes + hit.nbytes + idr.nbytes + ctypes.sizeof(pk.profiles) + inst.nbytes
+        d2h = part.summaries.nbytes
+    T = sum(times)
+    import torch.distributed as dist
+
+    t = torch.tensor([T], dtype=torch.float64, device="cuda")
+    if dist.is_available() and dist.is_initialized():
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return {"value": reqs * world / float(t.item()), "unit": "simulated requests/s", "h2d_bytes_per_step": h2d,
+            "d2h_bytes_per_step": d2h, "entry_point": "slosim_run_batch_host (C-ABI, host buffers)"}
+
+
+def cpu_baseline(args, host_summ, slice_id, slice_n):
+    """C oracle (port) on all host threads over a stride sample of one timed slice; bit-exact check."""
+    from oracle import oracle
+
+    threads = os.cpu_count() or 1
+    n_total = N_CONFIG5 if args.workload == "config5" else (3072 if args.workload == "config3" else 2)
+    # calibrate the sample to ~cpu_sample_s seconds: ~40k req/s per core for the port
+    target = int(args.cpu_sample_s * 40_000 * threads / 1000)
+    k = max(2, min(slice_n, target))
+    sel = slice_id * slice_n + np.sort(np.random.default_rng(slice_id).choice(slice_n, k, replace=False))
+    if args.workload == "config2":
+        sel = np.arange(2)
+    sw = build_workload(args.workload, synth=oracle.synth, select=sel)
+    t0 = time.perf_counter()
+    oracle.run_batch(sw.packed, threads=threads)
+    dt = time.perf_counter() - t0
+    ref = sw.packed.summaries
+    got = host_summ[sel]
+    mism = 0
+    for name in ref.dtype.names:
+        a, b = got[name], ref[name]
+        eq = np.array_equal(a, b, equal_nan=True) if a.dtype.kind == "f" else np.array_equal(a, b)
+        mism += 0 if eq else 1
+    cpu = {"value": sw.packed.n_requests / dt, "unit": "simulated requests/s", "cores": threads, "kind": "port",
+           "sample": f"{len(sel)} instances (seeded random sample of timed slice {slice_id}), "
+                     f"{sw.packed.n_requests} requests, {dt:.1f} s"}
+    parity = {"instances_checked": int(len(sel)), "fields_mismatched": int(mism),
+              "exact": mism == 0, "against": "C oracle (pinned to reference golden vectors)"}
+    return cpu, parity
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -243,6 +243,12 @@ int slosim_request_metrics(int64_t n, const int64_t* arrival, const int64_t* out
                            int64_t tpot_slo_us, int64_t* ttft_us, double* mean_tpot, double* tps,
                            uint8_t* met_flags, int32_t* misses, double* agg /* [5]: att x3, p50, p90 */);
 
+/* K6 pre-collective step: hist[cell[k]][e2e_met of instance k] += 1 over a device
+ * summary array (int64 histogram, DEVICE pointers, stream-ordered).  The histogram is
+ * then summed across GPUs with an integer all-reduce (bit-exact in any order). */
+int slosim_histogram(int64_t n, const slosim_summary_t* d_summaries, const int32_t* d_cell, int32_t n_bins,
+                     int64_t* d_hist, void* stream);
+
 /* Library identity (ABI version, sm arch compiled for) and visible CUDA devices. */
 int slosim_abi_version(void);
 int slosim_device_count(void);

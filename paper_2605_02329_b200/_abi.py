@@ -221,6 +221,7 @@ def lib():
                                        c_int32, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp]
     L.slosim_prefill_batch_us.argtypes = [c_int32, vp, vp, c_int32, vp, vp, vp]
     L.slosim_request_metrics.argtypes = [c_int64, vp, vp, vp, vp, c_int64, c_int64, vp, vp, vp, vp, vp, vp]
+    L.slosim_histogram.argtypes = [c_int64, vp, vp, c_int32, vp, vp]
     L.slosim_abi_version.restype = c_int
     L.slosim_last_error.restype = c_char_p
     L.slosim_build_info.restype = c_char_p
@@ -245,6 +246,7 @@ HEADER_SYMBOLS = [
     "slosim_select_decode",
     "slosim_prefill_batch_us",
     "slosim_request_metrics",
+    "slosim_histogram",
     "slosim_abi_version",
     "slosim_device_count",
     "slosim_build_info",

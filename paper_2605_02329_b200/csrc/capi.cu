@@ -749,6 +749,26 @@ extern "C" int slosim_synth_profile(slosim_profile_t* profile, int32_t n_anchors
     return SLOSIM_OK;
 }
 
+// K6 (pre-collective): per-cell histograms of e2e-met counts, accumulated on the device.
+__global__ void k_histogram(int64_t n, const slosim_summary_t* s, const int32_t* cell, int32_t n_bins,
+                            unsigned long long* hist) {
+    int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (k >= n || cell[k] < 0) return;
+    int b = s[k].e2e_met;
+    b = b < 0 ? 0 : (b >= n_bins ? n_bins - 1 : b);
+    atomicAdd(hist + (int64_t)cell[k] * n_bins + b, 1ULL);
+}
+
+extern "C" int slosim_histogram(int64_t n, const slosim_summary_t* d_summaries, const int32_t* d_cell,
+                                int32_t n_bins, int64_t* d_hist, void* stream) {
+    if (n < 0 || n_bins < 1) return SLOSIM_EINVAL;
+    if (n == 0) return SLOSIM_OK;
+    k_histogram<<<(unsigned)((n + 255) / 256), 256, 0, (cudaStream_t)stream>>>(n, d_summaries, d_cell, n_bins,
+                                                                              (unsigned long long*)d_hist);
+    CK(cudaGetLastError());
+    return SLOSIM_OK;
+}
+
 extern "C" int slosim_abi_version(void) { return SLOSIM_ABI_VERSION; }
 
 extern "C" int slosim_device_count(void) {
