@@ -187,7 +187,7 @@ assert ctypes.sizeof(Summary) == 136
 assert ctypes.sizeof(Instance) == 128
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libslosim_b200.so")
+LIB_PATH = os.environ.get("SLOSIM_LIB") or os.path.join(_HERE, "libslosim_b200.so")
 _lib = None
 
 

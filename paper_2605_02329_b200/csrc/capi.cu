@@ -78,7 +78,7 @@ extern "C" int64_t slosim_workspace_bytes(const slosim_batch_t* b) {
     int grid = 0;
     if (launch_geometry(b->n_instances, &grid) != SLOSIM_OK) return -1;
     return (int64_t)grid * 4 * (int64_t)ws_bytes(b->max_requests) +
-           (int64_t)b->n_profiles * 2 * (int64_t)sizeof(ProfTab);
+           (int64_t)b->n_profiles * 2 * (int64_t)sizeof(LutMem);
 }
 
 extern "C" int slosim_run_batch(const slosim_batch_t* b, void* stream) {
@@ -106,10 +106,10 @@ extern "C" int slosim_run_batch(const slosim_batch_t* b, void* stream) {
     size_t stride = ws_bytes(cap);
     size_t total = stride * (size_t)grid * 4;
     CK(g_ws.reserve(total));
-    CK(g_tabs.reserve(sizeof(ProfTab) * 2 * (size_t)b->n_profiles));
+    CK(g_tabs.reserve(sizeof(LutMem) * 2 * (size_t)b->n_profiles));
     CK(g_work.reserve(64));
-    ProfTab* sched = (ProfTab*)g_tabs.ptr;
-    ProfTab* frozen = sched + b->n_profiles;
+    LutMem* sched = (LutMem*)g_tabs.ptr;
+    LutMem* frozen = sched + b->n_profiles;
     build_profile_tables<<<b->n_profiles, 32, 0, st>>>(b->profiles, b->n_profiles, sched, frozen);
     CK(cudaGetLastError());
     CK(cudaMemsetAsync(g_work.ptr, 0, 8, st));
@@ -211,32 +211,17 @@ extern "C" int slosim_run_batch_host(const slosim_batch_t* hb, float* elapsed_ms
 // ------------------------------------------------------- snapshot kernels --
 namespace {
 
-// A framed LUT table in device scratch, built by one warp (lane = row).
-__device__ void snap_build_lut(int nb, int ns, const int32_t* bb, const int32_t* sb, const double* fsums,
-                               const int32_t* fcounts, ProfTab* tab, int lane) {
-    uint32_t rm = 0;
-    build_lut_table(nb, ns, bb, sb, fsums, fcounts, tab->sum, tab->mean, tab->slope, tab->cnt, tab->colmask, &rm,
-                    lane);
-    if (lane == 0) { tab->rowmask = rm; tab->empty = rm == 0; }
-    __syncwarp();
-}
-
 struct SnapLut {
     int nb, ns;
     int32_t bb[SLOSIM_MAX_BSZ_BUCKETS];
     int32_t sb[SLOSIM_MAX_SEQ_BUCKETS];
 };
 
-__global__ void k_lut_lookup(SnapLut sl, const double* fsums, const int32_t* fcounts, ProfTab* tab, int64_t n,
+__global__ void k_lut_lookup(SnapLut sl, const double* fsums, const int32_t* fcounts, LutMem* tab, int64_t n,
                              const int64_t* bsz, const int64_t* seq, double* out) {
-    __shared__ SnapLut s;
-    if (threadIdx.x == 0) s = sl;
+    if (threadIdx.x < 32) lut_build(tab, sl.nb, sl.ns, sl.bb, sl.sb, fsums, fcounts, threadIdx.x);
     __syncthreads();
-    if (threadIdx.x < 32) snap_build_lut(s.nb, s.ns, s.bb, s.sb, fsums, fcounts, tab, threadIdx.x);
-    __syncthreads();
-    __threadfence_block();
-    DLut L{s.nb, s.ns, s.bb, s.sb, tab->sum, tab->mean, tab->slope, tab->cnt, tab->colmask, tab->rowmask};
-    for (int64_t k = threadIdx.x; k < n; k += blockDim.x) out[k] = lut_lookup(L, bsz[k], seq[k]);
+    for (int64_t k = threadIdx.x; k < n; k += blockDim.x) out[k] = lut_lookup(tab, bsz[k], seq[k]);
 }
 
 __global__ void k_formula(int nbase, const int64_t* bx, const double* by, double gamma, int64_t n, const int64_t* bsz,
@@ -276,11 +261,11 @@ __device__ void snap_queue(int n, const int64_t* arr, const int32_t* inp, const 
                 bool less = arr[j] < arr[i] || (arr[j] == arr[i] && idr[j] < idr[i]);
                 rank += less;
             }
-            w.q_pos[rank] = i;
-            w.q_arr[rank] = arr[i];
-            w.q_inp[rank] = inp[i];
-            w.q_rem[rank] = (int32_t)rem[i];
-            w.q_full[rank] = (int32_t)rem[i];
+            w.i32(Q_POS)[rank] = i;
+            w.i64(Q_ARR)[rank] = arr[i];
+            w.i32(Q_INP)[rank] = inp[i];
+            w.i32(Q_REM)[rank] = (int32_t)rem[i];
+            w.i32(Q_FULL)[rank] = (int32_t)rem[i];
         }
     }
     __syncwarp();
@@ -291,40 +276,42 @@ __global__ void k_select_prefill(int policy, int n, const int64_t* arr, const in
                                  int64_t ttft, char* wsb, int64_t cap, int32_t* out_index, int64_t* out_take,
                                  int32_t* n_out, double* out_scores) {
     int lane = threadIdx.x;
-    WS w = carve_ws(wsb, cap);
+    WS w = make_ws(wsb, cap);
     snap_queue(n, arr, inp, rem, idr, w, lane);
-    int k = prefill_select(policy, w, 0, n, budget, t_now, tok, busy, ttft, w.pf_qidx, w.pf_take, lane);
-    for (int e = lane; e < k; e += 32) { out_index[e] = w.q_pos[w.pf_qidx[e]]; out_take[e] = w.pf_take[e]; }
+    int k = prefill_select(policy, w, 0, n, budget, t_now, tok, busy, ttft, lane);
+    const int32_t* q_pos = w.i32(Q_POS);
+    for (int e = lane; e < k; e += 32) { out_index[e] = q_pos[w.i32(PF_QIDX)[e]]; out_take[e] = w.i32(PF_TAKE)[e]; }
     if (policy == SLOSIM_PREFILL_KAIROS_URGENCY && out_scores)
-        for (int q = lane; q < n; q += 32) out_scores[w.q_pos[q]] = w.q_score[q];
+        for (int q = lane; q < n; q += 32) out_scores[q_pos[q]] = w.f64(Q_SCORE)[q];
     if (lane == 0) *n_out = k;
 }
 
 __global__ void k_select_decode(int policy, int n, const int64_t* seq, const int32_t* idr, const int64_t* ngen,
                                 const double* tfirst, double t_now, int64_t tpot, SnapLut sl, const double* fsums,
-                                const int32_t* fcounts, ProfTab* tab, char* wsb, int64_t cap, int32_t* out_batch,
+                                const int32_t* fcounts, LutMem* tab, char* wsb, int64_t cap, int32_t* out_batch,
                                 int32_t* n_batch, int32_t* out_delayed, int32_t* n_delayed, double* out_times,
                                 double* out_pred, double* out_smin, int32_t* out_fb) {
-    __shared__ SnapLut s;
     int lane = threadIdx.x;
-    if (lane == 0) s = sl;
-    __syncwarp();
-    snap_build_lut(s.nb, s.ns, s.bb, s.sb, fsums, fcounts, tab, lane);
-    DLut L{s.nb, s.ns, s.bb, s.sb, tab->sum, tab->mean, tab->slope, tab->cnt, tab->colmask, tab->rowmask};
-    WS w = carve_ws(wsb, cap);
+    lut_build(tab, sl.nb, sl.ns, sl.bb, sl.sb, fsums, fcounts, lane);
+    const LutMem* L = tab;
+    WS w = make_ws(wsb, cap);
+    int32_t* a_seq = w.i32(A_SEQ);
+    int32_t* a_idr = w.i32(A_IDR);
+    int32_t* a_flag = w.i32(A_FLAG);
+    int32_t* a_ord = w.i32(A_ORD);
     int64_t mx = 0;
     for (int i = lane; i < n; i += 32) {
-        w.a_seq[i] = (int32_t)seq[i];
-        w.a_idr[i] = idr[i];
-        w.a_flag[i] = 0;
+        a_seq[i] = (int32_t)seq[i];
+        a_idr[i] = idr[i];
+        a_flag[i] = 0;
         mx = seq[i] > mx ? seq[i] : mx;
     }
     mx = wmax64(mx);
     __syncwarp();
-    decode_order(n, w.a_seq, w.a_idr, w.a_ord, lane);
+    decode_order(n, a_seq, a_idr, a_ord, lane);
     double fallback = lut_lookup(L, n, mx);
     if (policy == SLOSIM_DECODE_CONTINUOUS) {
-        for (int r = lane; r < n; r += 32) out_batch[r] = w.a_ord[r];
+        for (int r = lane; r < n; r += 32) out_batch[r] = a_ord[r];
         if (lane == 0) {
             *n_batch = n; *n_delayed = 0; *out_pred = fallback;
             *out_smin = __longlong_as_double(0x7ff0000000000000LL);
@@ -343,11 +330,10 @@ __global__ void k_select_decode(int policy, int n, const int64_t* seq, const int
     double tcur;
     int64_t ms;
     int nd = 0;
-    int b = decode_scan(L, n, w.a_ord, w.a_seq, w.a_flag, smin, &tcur, &ms, out_batch, out_delayed, out_times, &nd,
-                        lane);
+    int b = decode_scan(L, n, a_ord, a_seq, a_flag, smin, &tcur, &ms, out_batch, out_delayed, out_times, &nd, lane);
     __syncwarp();
     if (b == 0) {
-        for (int r = lane; r < n; r += 32) out_batch[r] = w.a_ord[r];
+        for (int r = lane; r < n; r += 32) out_batch[r] = a_ord[r];
         if (lane == 0) { *n_batch = n; *n_delayed = 0; *out_pred = fallback; *out_smin = smin; *out_fb = 1; }
     } else if (lane == 0) {
         *n_batch = b; *n_delayed = nd; *out_pred = tcur; *out_smin = smin; *out_fb = 0;
@@ -521,9 +507,9 @@ extern "C" int slosim_lut_lookup(int32_t nb, const int32_t* bb, int32_t ns, cons
     std::vector<double> fs;
     std::vector<int32_t> fc;
     frame(nb, ns, sums, counts, fs, fc);
-    CK(snap_reserve(sizeof(ProfTab) + fs.size() * 12 + (size_t)n * 24 + 4096));
+    CK(snap_reserve(sizeof(LutMem) + fs.size() * 12 + (size_t)n * 24 + 4096));
     Bump bp{(char*)g_snap.ptr};
-    ProfTab* tab = bp.take<ProfTab>(1);
+    LutMem* tab = bp.take<LutMem>(1);
     double* dfs = bp.take<double>(fs.size());
     int32_t* dfc = bp.take<int32_t>(fc.size());
     int64_t* db = bp.take<int64_t>(n);
@@ -636,10 +622,10 @@ extern "C" int slosim_select_decode(int32_t policy, int32_t n, const int64_t* se
     std::vector<int32_t> fc;
     frame(nb, ns, sums, counts, fs, fc);
     size_t wsb = ws_bytes(n);
-    CK(snap_reserve(wsb + sizeof(ProfTab) + fs.size() * 12 + (size_t)n * 64 + 8192));
+    CK(snap_reserve(wsb + sizeof(LutMem) + fs.size() * 12 + (size_t)n * 64 + 8192));
     Bump bp{(char*)g_snap.ptr};
     char* dws = bp.take<char>(wsb);
-    ProfTab* tab = bp.take<ProfTab>(1);
+    LutMem* tab = bp.take<LutMem>(1);
     double* dfs = bp.take<double>(fs.size());
     int32_t* dfc = bp.take<int32_t>(fc.size());
     int64_t* dseq = bp.take<int64_t>(n);

@@ -5,14 +5,15 @@
 // from an atomic work counter.  All control flow is warp-uniform: every lane
 // holds the same scalar state (time, pool status, counters) and the lanes
 // cooperate on the per-request sets (prefill queue, pending admission list,
-// active decode set) which live in a per-warp SoA workspace.
+// active decode set), which live in a per-warp SoA workspace that stays
+// L1-resident for the life of an instance.
 //
 // Reference mapping (engine.py):
-//   instant loop :264-271      -> simulate() main loop
-//   _dispatch    :286-302      -> absorb_arrivals / absorb_transfers / finish_* below
+//   instant loop :264-271                      -> simulate() main loop
+//   _dispatch :286-302                         -> arrival / transfer / completion blocks
 //   _start_prefill / _finish_prefill_step :307-350
 //   _admit :355-375, _start_decode / _finish_decode_step :377-413
-//   metrics :274-284 -> metrics.py:30-144 (online per-request rows, finalize())
+//   metrics :274-284 -> metrics.py:30-144      (per-request rows at retirement, finalize)
 #pragma once
 #include "../../include/slosim_b200.h"
 #include "lut.cuh"
@@ -52,121 +53,49 @@ __device__ __forceinline__ int64_t wscan_incl64(int64_t v, int lane) {
     for (int o = 1; o < 32; o <<= 1) { int64_t w = __shfl_up_sync(FULLMASK, v, o); if (lane >= o) v += w; }
     return v;
 }
+__device__ __forceinline__ unsigned lanemask_lt(int lane) { return (1u << lane) - 1u; }
 
 // ------------------------------------------------------------- workspace --
-// Per-warp SoA workspace, capacity `cap` requests (the largest instance of the
-// batch).  Carved from one global allocation by carve_ws().
-struct WS {
-    // prefill queue [qh, qt): requests that arrived and still have prefill work,
-    // in trace position order == (arrival, id) order (prefill_sched.py:35-36)
-    int32_t *q_pos, *q_rem, *q_full, *q_inp;
-    int64_t *q_arr;
-    double* q_score;
-    // in-flight prefill batch (queue index, take), batch order
-    int32_t *pf_qidx, *pf_take;
-    // in-flight transfers, push order (engine.py:346-349)
-    int64_t *tr_t, *tr_tpf;
-    int32_t* tr_pos;
-    // pending admission list sorted by (t_prefill_finish, id) (engine.py:358)
-    int64_t *pd_tpf, *pd_ttr;
-    int32_t *pd_pos, *pd_idr;
-    // active decode set (engine.py:374); a_flag bit0 = in the running batch, bit1 = ttft met
-    int32_t *a_pos, *a_seq, *a_idr, *a_out, *a_inp, *a_miss, *a_flag, *a_ord;
-    int64_t* a_tfirst;
-    // decode tps of retired requests (metrics.py:49-54) for the percentile select
-    double* tps;
-    // mutable LUT copy [K] + colmask [16]
-    double *l_sum, *l_mean, *l_slope;
-    int32_t* l_cnt;
-    uint64_t* l_colmask;
-};
+// Per-warp SoA workspace of capacity `cap` requests, addressed as base + fixed
+// multiples of the two aligned array sizes (so it costs 3 live registers).
+enum WsI32 { Q_POS, Q_REM, Q_FULL, Q_INP, PF_QIDX, PF_TAKE, TR_POS, PD_POS, PD_IDR,
+             A_POS, A_SEQ, A_IDR, A_OUT, A_INP, A_MISS, A_FLAG, A_ORD, N_WS_I32 };
+enum WsI64 { Q_ARR, Q_SCORE, TR_T, TR_TPF, PD_TPF, PD_TTR, A_TFIRST, TPS, N_WS_I64 };
 
 __host__ __device__ inline size_t ws_align(size_t x) { return (x + 127) & ~(size_t)127; }
 
-__host__ __device__ inline size_t ws_bytes(int64_t cap) {
-    size_t c = (size_t)(cap > 0 ? cap : 1);
-    size_t b = 0;
-    b += 4 * ws_align(4 * c) + 2 * ws_align(8 * c);      // queue
-    b += 2 * ws_align(4 * c);                            // pf
-    b += 2 * ws_align(8 * c) + ws_align(4 * c);          // transfers
-    b += 2 * ws_align(8 * c) + 2 * ws_align(4 * c);      // pending
-    b += 8 * ws_align(4 * c) + ws_align(8 * c);          // active
-    b += ws_align(8 * c);                                // tps
-    const size_t K = SLOSIM_MAX_BSZ_BUCKETS * SLOSIM_MAX_SEQ_BUCKETS;
-    b += 3 * ws_align(8 * K) + ws_align(4 * K) + ws_align(8 * SLOSIM_MAX_BSZ_BUCKETS);
-    return b;
-}
-
-__device__ inline WS carve_ws(char* base, int64_t cap) {
-    size_t c = (size_t)(cap > 0 ? cap : 1);
-    const size_t K = SLOSIM_MAX_BSZ_BUCKETS * SLOSIM_MAX_SEQ_BUCKETS;
-    WS w;
-    char* p = base;
-#define TAKE(field, type, count) do { w.field = (type*)p; p += ws_align(sizeof(type) * (count)); } while (0)
-    TAKE(q_pos, int32_t, c); TAKE(q_rem, int32_t, c); TAKE(q_full, int32_t, c); TAKE(q_inp, int32_t, c);
-    TAKE(q_arr, int64_t, c); TAKE(q_score, double, c);
-    TAKE(pf_qidx, int32_t, c); TAKE(pf_take, int32_t, c);
-    TAKE(tr_t, int64_t, c); TAKE(tr_tpf, int64_t, c); TAKE(tr_pos, int32_t, c);
-    TAKE(pd_tpf, int64_t, c); TAKE(pd_ttr, int64_t, c); TAKE(pd_pos, int32_t, c); TAKE(pd_idr, int32_t, c);
-    TAKE(a_pos, int32_t, c); TAKE(a_seq, int32_t, c); TAKE(a_idr, int32_t, c); TAKE(a_out, int32_t, c);
-    TAKE(a_inp, int32_t, c); TAKE(a_miss, int32_t, c); TAKE(a_flag, int32_t, c); TAKE(a_ord, int32_t, c);
-    TAKE(a_tfirst, int64_t, c);
-    TAKE(tps, double, c);
-    TAKE(l_sum, double, K); TAKE(l_mean, double, K); TAKE(l_slope, double, K); TAKE(l_cnt, int32_t, K);
-    TAKE(l_colmask, uint64_t, SLOSIM_MAX_BSZ_BUCKETS);
-#undef TAKE
-    return w;
-}
-
-// Per-profile precomputed LUT tables (means/slopes/masks), built once per batch.
-struct ProfTab {
-    double sum[SLOSIM_MAX_BSZ_BUCKETS * SLOSIM_MAX_SEQ_BUCKETS];
-    double mean[SLOSIM_MAX_BSZ_BUCKETS * SLOSIM_MAX_SEQ_BUCKETS];
-    double slope[SLOSIM_MAX_BSZ_BUCKETS * SLOSIM_MAX_SEQ_BUCKETS];
-    int32_t cnt[SLOSIM_MAX_BSZ_BUCKETS * SLOSIM_MAX_SEQ_BUCKETS];
-    uint64_t colmask[SLOSIM_MAX_BSZ_BUCKETS];
-    uint32_t rowmask;
-    int32_t empty;
+struct WS {
+    char* base;
+    uint32_t a4, a8;
+    __device__ __forceinline__ int32_t* i32(int k) const { return (int32_t*)(base + (size_t)k * a4); }
+    __device__ __forceinline__ int64_t* i64(int k) const {
+        return (int64_t*)(base + (size_t)N_WS_I32 * a4 + (size_t)k * a8);
+    }
+    __device__ __forceinline__ double* f64(int k) const { return (double*)i64(k); }
+    __device__ __forceinline__ LutMem* lut() const {
+        return (LutMem*)(base + (size_t)N_WS_I32 * a4 + (size_t)N_WS_I64 * a8);
+    }
 };
 
-// Build one LUT table from a 16x64-framed (sums, counts) pair; one warp.
-__device__ void build_lut_table(int nb, int ns, const int32_t* bb, const int32_t* sb, const double* fsums,
-                                const int32_t* fcounts, double* sum, double* mean, double* slope, int32_t* cnt,
-                                uint64_t* colmask, uint32_t* rowmask_out, int lane) {
-    for (int c = lane; c < nb * ns; c += 32) {
-        int i = c / ns, j = c % ns;
-        sum[c] = fsums[i * SLOSIM_MAX_SEQ_BUCKETS + j];
-        cnt[c] = fcounts[i * SLOSIM_MAX_SEQ_BUCKETS + j];
-        mean[c] = 0.0;
-        slope[c] = 0.0;
-    }
-    __syncwarp();
-    DLut L{nb, ns, bb, sb, sum, mean, slope, cnt, colmask, 0u};
-    if (lane < nb) lut_build_row(L, lane);
-    __syncwarp();
-    bool pop = lane < nb && colmask[lane] != 0;
-    uint32_t rm = __ballot_sync(FULLMASK, pop);
-    if (rowmask_out) *rowmask_out = rm;
+__host__ __device__ inline size_t ws_bytes(int64_t cap) {
+    size_t c = (size_t)(cap > 0 ? cap : 1);
+    return N_WS_I32 * ws_align(4 * c) + N_WS_I64 * ws_align(8 * c) + ws_align(sizeof(LutMem));
 }
 
-__global__ void build_profile_tables(const slosim_profile_t* profiles, int n_profiles, ProfTab* sched,
-                                     ProfTab* frozen) {
+__device__ __forceinline__ WS make_ws(char* base, int64_t cap) {
+    size_t c = (size_t)(cap > 0 ? cap : 1);
+    return WS{base, (uint32_t)ws_align(4 * c), (uint32_t)ws_align(8 * c)};
+}
+
+// Per-profile LUT tables (scheduler seed + frozen ground truth), built once per launch.
+__global__ void build_profile_tables(const slosim_profile_t* profiles, int n_profiles, LutMem* sched,
+                                     LutMem* frozen) {
     int lane = threadIdx.x & 31;
     int p = blockIdx.x;
     if (p >= n_profiles) return;
     const slosim_profile_t* P = profiles + p;
-    uint32_t rm = 0;
-    build_lut_table(P->nb, P->ns, P->bsz_buckets, P->seq_buckets, P->lut_sums, P->lut_counts, sched[p].sum,
-                    sched[p].mean, sched[p].slope, sched[p].cnt, sched[p].colmask, &rm, lane);
-    if (lane == 0) { sched[p].rowmask = rm; sched[p].empty = rm == 0; }
-    build_lut_table(P->nb, P->ns, P->bsz_buckets, P->seq_buckets, P->gt_sums, P->gt_counts, frozen[p].sum,
-                    frozen[p].mean, frozen[p].slope, frozen[p].cnt, frozen[p].colmask, &rm, lane);
-    if (lane == 0) { frozen[p].rowmask = rm; frozen[p].empty = rm == 0; }
-}
-
-__device__ __forceinline__ DLut lut_view(const slosim_profile_t* P, const ProfTab* T) {
-    return DLut{P->nb, P->ns, P->bsz_buckets, P->seq_buckets, (double*)T->sum, (double*)T->mean,
-                (double*)T->slope, (int32_t*)T->cnt, (uint64_t*)T->colmask, T->rowmask};
+    lut_build(sched + p, P->nb, P->ns, P->bsz_buckets, P->seq_buckets, P->lut_sums, P->lut_counts, lane);
+    lut_build(frozen + p, P->nb, P->ns, P->bsz_buckets, P->seq_buckets, P->gt_sums, P->gt_counts, lane);
 }
 
 // ------------------------------------------------------------ trace writer --
@@ -213,16 +142,50 @@ __device__ void decode_order(int an, const int32_t* a_seq, const int32_t* a_idr,
 // Alg. 3 greedy scan (select_decode_batch decode_sched.py:80-111) over the
 // ordered active set.  Lanes test 32 consecutive candidates speculatively
 // against the current (|B|, t_cur); the first admissible one is admitted and
-// the scan restarts right after it.  Sets a_flag bit0 of the admitted entries.
-// Returns |B| (0 = fallback); *tcur_out = t_cur, *maxseq_out = seq of last admitted.
-// Optional audit outputs (snapshot API): admitted order, delayed order, admission times.
-__device__ int decode_scan(const DLut& L, int an, const int32_t* ord, const int32_t* a_seq, int32_t* a_flag,
+// the scan restarts right after it; a round with no admissible lane rejects
+// all remaining candidates of the window at once.  On a fully populated LUT
+// the per-candidate column selection is computed once and each round only
+// selects the rows for |B|+1.  Sets a_flag bit0 of admitted entries; returns
+// |B| (0 = fallback).  Optional audit outputs (snapshot API): admitted order,
+// delayed order, admission times.
+__device__ int decode_scan(const LutMem* L, int an, const int32_t* ord, const int32_t* a_seq, int32_t* a_flag,
                            double smin, double* tcur_out, int64_t* maxseq_out, int32_t* audit_batch,
                            int32_t* audit_delayed, double* audit_times, int* n_delayed, int lane) {
     int b = 0;
     double tcur = 0.0;
     int64_t mseq = 0;
-    int s = 0, nd = 0;
+    int nd = 0;
+    if (L->full && an <= 32 && !audit_delayed) {
+        bool have = lane < an;
+        int i = have ? ord[lane] : 0;
+        int64_t seq = have ? a_seq[i] : 1;
+        ColSel cs = lut_col(L, seq);
+        int s = 0;
+        while (s < an) {
+            RowSel rs = lut_rows(L, b + 1);
+            double thr = b ? xdiv((double)b, tcur) : 0.0;
+            bool valid = lane >= s && have;
+            double ts = 0.0;
+            bool cond = false;
+            if (valid) {
+                ts = lut_eval(L, rs, cs);
+                cond = ts <= smin && (b == 0 || xdiv((double)(b + 1), ts) > thr);
+            }
+            unsigned m = __ballot_sync(FULLMASK, cond);
+            if (!m) break;
+            int j = __ffs((int)m) - 1;
+            if (lane == j) a_flag[i] |= 1;
+            tcur = __shfl_sync(FULLMASK, ts, j);
+            mseq = __shfl_sync(FULLMASK, seq, j);
+            b++;
+            s = j + 1;
+        }
+        __syncwarp();
+        *tcur_out = tcur;
+        *maxseq_out = mseq;
+        return b;
+    }
+    int s = 0;
     while (s < an) {
         int r = s + lane;
         bool valid = r < an;
@@ -238,7 +201,6 @@ __device__ int decode_scan(const DLut& L, int an, const int32_t* ord, const int3
         int j = m ? __ffs((int)m) - 1 : 32;
         int lim = an - s < 32 ? an - s : 32;
         if (audit_delayed) {
-            // rejected candidates in scan order
             if (lane < j && lane < lim) audit_delayed[nd + lane] = i;
             nd += (j < lim ? j : lim);
         }
@@ -274,7 +236,6 @@ __device__ __forceinline__ int64_t fcfs_walk_chunk(bool valid, int64_t arrival, 
         int64_t a2 = __shfl_up_sync(FULLMASK, A, o);
         int64_t b2 = __shfl_up_sync(FULLMASK, Bv, o);
         if (lane >= o) {
-            // earlier (a2, b2) composed with later (A, Bv)
             int64_t nb = b2 + A;
             Bv = nb > Bv ? nb : Bv;
             A = a2 + A;
@@ -296,8 +257,10 @@ __device__ __forceinline__ double selection_score(int64_t ttft_slo, int64_t fini
 // Packs the chunk budget from the queue [qh, qt) per policy (prefill_sched.py:93-145).
 // Writes (queue index, take) in batch order; returns the number of entries.
 __device__ int prefill_select(int policy, const WS& w, int qh, int qt, int64_t budget, int64_t t_now,
-                              int64_t est_tok, int64_t est_busy, int64_t ttft_slo, int32_t* pf_qidx,
-                              int32_t* pf_take, int lane) {
+                              int64_t est_tok, int64_t est_busy, int64_t ttft_slo, int lane) {
+    int32_t* pf_qidx = w.i32(PF_QIDX);
+    int32_t* pf_take = w.i32(PF_TAKE);
+    const int32_t* q_rem = w.i32(Q_REM);
     int k = 0;
     int64_t left = budget;
     if (policy == SLOSIM_PREFILL_FCFS) {
@@ -305,14 +268,15 @@ __device__ int prefill_select(int policy, const WS& w, int qh, int qt, int64_t b
         for (int base = qh; base < qt && left > 0; base += 32) {
             int qi = base + lane;
             bool valid = qi < qt;
-            int64_t rem = valid ? w.q_rem[qi] : 0;
+            int64_t rem = valid ? q_rem[qi] : 0;
             int64_t incl = wscan_incl64(rem, lane);
             int64_t excl = incl - rem;
             int64_t take = (valid && excl < left) ? (rem < left - excl ? rem : left - excl) : 0;
             unsigned m = __ballot_sync(FULLMASK, take > 0);
             if (take > 0) {
-                int d = k + __popc(m & ((1u << lane) - 1u));
-                pf_qidx[d] = qi; pf_take[d] = (int32_t)take;
+                int d = k + __popc(m & lanemask_lt(lane));
+                pf_qidx[d] = qi;
+                pf_take[d] = (int32_t)take;
             }
             k += __popc(m);
             left -= wsum64(take);
@@ -320,18 +284,21 @@ __device__ int prefill_select(int policy, const WS& w, int qh, int qt, int64_t b
         __syncwarp();
         return k;
     }
+    double* q_score = w.f64(Q_SCORE);
     if (policy == SLOSIM_PREFILL_KAIROS_URGENCY) {
         // predict_finish_times + _selection_score for every queued request
+        const int64_t* q_arr = w.i64(Q_ARR);
+        const int32_t* q_inp = w.i32(Q_INP);
         int64_t cursor = t_now;
         for (int base = qh; base < qt; base += 32) {
             int qi = base + lane;
             bool valid = qi < qt;
-            int64_t a = valid ? w.q_arr[qi] : 0;
-            int64_t rem = valid ? w.q_rem[qi] : 0;
+            int64_t a = valid ? q_arr[qi] : 0;
+            int64_t rem = valid ? q_rem[qi] : 0;
             int64_t d = valid ? ceil_muldiv(rem, est_busy, est_tok) : 0;
             int nvalid = qt - base < 32 ? qt - base : 32;
             int64_t fin = fcfs_walk_chunk(valid, a, d, cursor, nvalid, lane);
-            if (valid) w.q_score[qi] = selection_score(ttft_slo, fin, a, w.q_inp[qi]);
+            if (valid) q_score[qi] = selection_score(ttft_slo, fin, a, q_inp[qi]);
         }
         __syncwarp();
     }
@@ -346,8 +313,7 @@ __device__ int prefill_select(int policy, const WS& w, int qh, int qt, int64_t b
         for (int base = qh; base < qt; base += 32) {
             int qi = base + lane;
             if (qi < qt) {
-                uint64_t key = policy == SLOSIM_PREFILL_SJF ? (uint64_t)(uint32_t)w.q_rem[qi]
-                                                            : ~dkey(w.q_score[qi]);
+                uint64_t key = policy == SLOSIM_PREFILL_SJF ? (uint64_t)(uint32_t)q_rem[qi] : ~dkey(q_score[qi]);
                 bool after = key > pk || (key == pk && qi > pq);
                 if (after && (key < bk || (key == bk && qi < bq))) { bk = key; bq = qi; }
             }
@@ -356,7 +322,7 @@ __device__ int prefill_select(int policy, const WS& w, int qh, int qt, int64_t b
         int cand = (bk == mk) ? bq : 0x7fffffff;
         int mq = __reduce_min_sync(FULLMASK, cand);
         if (mq == 0x7fffffff) break;
-        int64_t rem = w.q_rem[mq];
+        int64_t rem = q_rem[mq];
         int64_t take = rem < left ? rem : left;
         if (take > 0) {
             if (lane == 0) { pf_qidx[k] = mq; pf_take[k] = (int32_t)take; }
@@ -373,8 +339,8 @@ __device__ int prefill_select(int policy, const WS& w, int qh, int qt, int64_t b
 // --------------------------------------------------------------- engine --
 struct Ctx {
     slosim_batch_t B;  // by value: lives in the kernel parameter (constant) bank
-    const ProfTab* sched_tab;
-    const ProfTab* frozen_tab;
+    const LutMem* sched_tab;
+    const LutMem* frozen_tab;
 };
 
 __device__ __forceinline__ int64_t arrival_of(const int64_t* Tarr, double fac, int p) {
@@ -385,27 +351,32 @@ __device__ __forceinline__ int64_t arrival_of(const int64_t* Tarr, double fac, i
 // Pending list insert keeping (tpf, id_rank) order (engine.py:358).
 __device__ void pending_insert(const WS& w, int ph, int& pt, int64_t tpf, int32_t idr, int64_t ttr, int32_t pos,
                                int lane) {
-    // position = number of entries with key < new key
-    int cnt = 0;
-    for (int base = ph; base < pt; base += 32) {
-        int k = base + lane;
-        bool less = k < pt && (w.pd_tpf[k] < tpf || (w.pd_tpf[k] == tpf && w.pd_idr[k] < idr));
-        cnt += __popc(__ballot_sync(FULLMASK, less));
+    int64_t* pd_tpf = w.i64(PD_TPF);
+    int64_t* pd_ttr = w.i64(PD_TTR);
+    int32_t* pd_pos = w.i32(PD_POS);
+    int32_t* pd_idr = w.i32(PD_IDR);
+    int at = pt;
+    if (pt > ph && (pd_tpf[pt - 1] > tpf || (pd_tpf[pt - 1] == tpf && pd_idr[pt - 1] > idr))) {
+        int cnt = 0;
+        for (int base = ph; base < pt; base += 32) {
+            int k = base + lane;
+            bool less = k < pt && (pd_tpf[k] < tpf || (pd_tpf[k] == tpf && pd_idr[k] < idr));
+            cnt += __popc(__ballot_sync(FULLMASK, less));
+        }
+        at = ph + cnt;
+        for (int hi = pt; hi > at; hi -= 32) {
+            int lo = hi - 32 > at ? hi - 32 : at;
+            int k = lo + lane;
+            int64_t a = 0, b = 0;
+            int32_t c = 0, d = 0;
+            bool v = k < hi;
+            if (v) { a = pd_tpf[k]; b = pd_ttr[k]; c = pd_pos[k]; d = pd_idr[k]; }
+            __syncwarp();
+            if (v) { pd_tpf[k + 1] = a; pd_ttr[k + 1] = b; pd_pos[k + 1] = c; pd_idr[k + 1] = d; }
+            __syncwarp();
+        }
     }
-    int at = ph + cnt;
-    // shift [at, pt) right by one, from the end, 32 at a time
-    for (int hi = pt; hi > at; hi -= 32) {
-        int lo = hi - 32 > at ? hi - 32 : at;
-        int k = lo + lane;
-        int64_t a = 0, b = 0;
-        int32_t c = 0, d = 0;
-        bool v = k < hi;
-        if (v) { a = w.pd_tpf[k]; b = w.pd_ttr[k]; c = w.pd_pos[k]; d = w.pd_idr[k]; }
-        __syncwarp();
-        if (v) { w.pd_tpf[k + 1] = a; w.pd_ttr[k + 1] = b; w.pd_pos[k + 1] = c; w.pd_idr[k + 1] = d; }
-        __syncwarp();
-    }
-    if (lane == 0) { w.pd_tpf[at] = tpf; w.pd_ttr[at] = ttr; w.pd_pos[at] = pos; w.pd_idr[at] = idr; }
+    if (lane == 0) { pd_tpf[at] = tpf; pd_ttr[at] = ttr; pd_pos[at] = pos; pd_idr[at] = idr; }
     pt++;
     __syncwarp();
 }
@@ -428,22 +399,32 @@ __device__ double radix_select(const double* v, int n, int64_t r, int lane) {
     return __longlong_as_double((long long)prefix);
 }
 
+__device__ void write_config_error(slosim_summary_t* out, int n) {
+    slosim_summary_t s = {};
+    s.status = SLOSIM_ECONFIG;
+    s.n = n;
+    s.tps_p50 = __longlong_as_double(0x7ff8000000000000LL);
+    s.tps_p90 = s.tps_p50;
+    *out = s;
+}
+
 __device__ void simulate(const Ctx& cx, int64_t ii, const WS& w, int lane) {
     const slosim_batch_t* B = &cx.B;
-    const slosim_instance_t I = B->instances[ii];
-    const slosim_profile_t* P = B->profiles + I.profile_id;
-    slosim_summary_t* out = B->summaries + ii;
-    const int n = I.n_requests;
-    const int64_t off = I.trace_offset;
+    const slosim_instance_t* I = B->instances + ii;
+    const int n = I->n_requests;
+    const int pid = I->profile_id;
+    const slosim_profile_t* P = B->profiles + pid;
+    const int64_t off = I->trace_offset;
     const int64_t* Tarr = B->traces.arrival_us + off;
     const int32_t* Tinp = B->traces.input_len + off;
     const int32_t* Tout = B->traces.output_len + off;
     const int32_t* Thit = B->traces.prefix_hit_len + off;
     const int32_t* Tidr = B->traces.id_rank + off;
-    const double fac = I.rescale_factor;
+    const double fac = I->rescale_factor;
     const bool rows = (B->flags & SLOSIM_F_ROWS) != 0;
-    const slosim_rows_t R = B->rows;
-    const int64_t tpot_slo = I.tpot_slo_us, ttft_slo = I.ttft_slo_us;
+    const int64_t tpot_slo = I->tpot_slo_us, ttft_slo = I->ttft_slo_us, kv_cap = I->kv_capacity_tokens;
+    const int ppol = I->prefill_policy, dpol = I->decode_policy;
+    const int64_t row0 = I->row_offset;
 
     // ---- Simulation.__init__ checks (engine.py:218-232)
     int64_t worst = 0;
@@ -452,38 +433,25 @@ __device__ void simulate(const Ctx& cx, int64_t ii, const WS& w, int lane) {
         worst = need > worst ? need : worst;
     }
     worst = wmax64(worst);
-    const ProfTab* ST = cx.sched_tab + I.profile_id;
-    if (worst > I.kv_capacity_tokens || ST->empty) {
-        if (lane == 0) {
-            slosim_summary_t s = {};
-            s.status = SLOSIM_ECONFIG;
-            s.n = n;
-            s.tps_p50 = __longlong_as_double(0x7ff8000000000000LL);
-            s.tps_p90 = s.tps_p50;
-            *out = s;
-        }
+    const LutMem* ST = cx.sched_tab + pid;
+    if (worst > kv_cap || ST->rowmask == 0) {
+        if (lane == 0) write_config_error(B->summaries + ii, n);
         return;
     }
-    const bool use_lut = I.decode_policy == SLOSIM_DECODE_KAIROS_SLACK ||
-                         (B->flags & (SLOSIM_F_ALWAYS_LUT | SLOSIM_F_EXPORT_LUT));
-    const int nb = P->nb, ns = P->ns, K = nb * ns;
-    DLut L{nb, ns, P->bsz_buckets, P->seq_buckets, w.l_sum, w.l_mean, w.l_slope, w.l_cnt, w.l_colmask, ST->rowmask};
-    if (use_lut) {
-        for (int c = lane; c < K; c += 32) {
-            w.l_sum[c] = ST->sum[c]; w.l_mean[c] = ST->mean[c]; w.l_slope[c] = ST->slope[c]; w.l_cnt[c] = ST->cnt[c];
-        }
-        if (lane < SLOSIM_MAX_BSZ_BUCKETS) w.l_colmask[lane] = ST->colmask[lane];
-        __syncwarp();
-    }
-    const DLut FZ = lut_view(P, cx.frozen_tab + I.profile_id);
-    const bool frozen = P->gt_frozen != 0;
-    const int n_base = P->n_base, n_curve = P->n_curve;
-    const double gamma = P->gamma, eps = P->noise_eps;
-    Pcg64 rng{I.rng_state_hi, I.rng_state_lo, I.rng_inc_hi, I.rng_inc_lo};
+    const bool use_lut = dpol == SLOSIM_DECODE_KAIROS_SLACK || (B->flags & (SLOSIM_F_ALWAYS_LUT | SLOSIM_F_EXPORT_LUT));
+    LutMem* L = w.lut();
+    if (use_lut) lut_copy(L, ST, lane);
     int64_t est_tok = P->est_tokens, est_busy = P->est_busy_us;
+    Pcg64 rng{I->rng_state_hi, I->rng_state_lo, I->rng_inc_hi, I->rng_inc_lo};
 
     TraceW T{nullptr, 0, 0};
-    if (B->trace_buf && I.trace_buf_offset >= 0) { T.buf = B->trace_buf + I.trace_buf_offset; T.cap = I.trace_buf_words; }
+    if (B->trace_buf && I->trace_buf_offset >= 0) { T.buf = B->trace_buf + I->trace_buf_offset; T.cap = I->trace_buf_words; }
+
+    int32_t* q_pos = w.i32(Q_POS);
+    int32_t* q_rem = w.i32(Q_REM);
+    int32_t* q_full = w.i32(Q_FULL);
+    int32_t* q_inp = w.i32(Q_INP);
+    int64_t* q_arr = w.i64(Q_ARR);
 
     int ai = 0;
     int64_t next_arr = n > 0 ? arrival_of(Tarr, fac, 0) : SLOSIM_INF64;
@@ -494,6 +462,8 @@ __device__ void simulate(const Ctx& cx, int64_t ii, const WS& w, int lane) {
     int64_t tr_min = SLOSIM_INF64;
     int ph = 0, pt = 0;
     int an = 0;
+    int64_t amax = 0;        // max seq_len over the active set
+    int dc_prefix = -1;      // >= 0: the running batch is active[0, dc_prefix) (continuous); -1: flags
     int64_t dc_end = SLOSIM_INF64, dc_dur = 0, dc_bsz = 0, dc_max = 0;
     int64_t kv = 0;
     int finished = 0;
@@ -520,7 +490,7 @@ __device__ void simulate(const Ctx& cx, int64_t ii, const WS& w, int lane) {
                     int qi = qt + lane;
                     int32_t inp = Tinp[p];
                     int32_t full = inp - Thit[p];
-                    w.q_pos[qi] = p; w.q_arr[qi] = a; w.q_inp[qi] = inp; w.q_full[qi] = full; w.q_rem[qi] = full;
+                    q_pos[qi] = p; q_arr[qi] = a; q_inp[qi] = inp; q_full[qi] = full; q_rem[qi] = full;
                     if (T.buf) {
                         int64_t o = T.used + 3 * lane;
                         T.put(o, SLOSIM_EV_ARRIVAL); T.put(o + 1, t); T.put(o + 2, p);
@@ -536,19 +506,22 @@ __device__ void simulate(const Ctx& cx, int64_t ii, const WS& w, int lane) {
 
         // ---- transfers due now that were pushed at earlier instants (engine.py:294-298)
         if (tr_min == t) {
+            int64_t* tr_t = w.i64(TR_T);
+            int64_t* tr_tpf = w.i64(TR_TPF);
+            int32_t* tr_pos = w.i32(TR_POS);
             int m_keep = 0;
             for (int base = 0; base < trn; base += 32) {
                 int k = base + lane;
                 bool v = k < trn;
-                int64_t tt = v ? w.tr_t[k] : 0, tpf = v ? w.tr_tpf[k] : 0;
-                int32_t pos = v ? w.tr_pos[k] : 0;
+                int64_t tt = v ? tr_t[k] : 0, tpf = v ? tr_tpf[k] : 0;
+                int32_t pos = v ? tr_pos[k] : 0;
                 bool due = v && tt == t;
                 unsigned dm = __ballot_sync(FULLMASK, due);
                 unsigned km = __ballot_sync(FULLMASK, v && !due);
                 __syncwarp();
                 if (v && !due) {
-                    int o = m_keep + __popc(km & ((1u << lane) - 1u));
-                    w.tr_t[o] = tt; w.tr_tpf[o] = tpf; w.tr_pos[o] = pos;
+                    int o = m_keep + __popc(km & lanemask_lt(lane));
+                    tr_t[o] = tt; tr_tpf[o] = tpf; tr_pos[o] = pos;
                 }
                 m_keep += __popc(km);
                 __syncwarp();
@@ -564,57 +537,55 @@ __device__ void simulate(const Ctx& cx, int64_t ii, const WS& w, int lane) {
             }
             trn = m_keep;
             int64_t mn = SLOSIM_INF64;
-            for (int k = lane; k < trn; k += 32) { int64_t tt = w.tr_t[k]; mn = tt < mn ? tt : mn; }
+            for (int k = lane; k < trn; k += 32) { int64_t tt = tr_t[k]; mn = tt < mn ? tt : mn; }
             tr_min = wmin64(mn);
         }
 
         // ---- prefill step completion (engine.py:327-350)
         if (pf_end == t) {
+            const int32_t* pf_qidx = w.i32(PF_QIDX);
+            const int32_t* pf_take = w.i32(PF_TAKE);
             int64_t tot = 0;
-            for (int base = 0; base < pf_k; base += 32) {
-                int e = base + lane;
-                int64_t take = 0;
-                if (e < pf_k) { take = w.pf_take[e]; w.q_rem[w.pf_qidx[e]] -= (int32_t)take; }
-                tot += take;
-            }
-            tot = wsum64(tot);
-            est_tok += tot;
-            est_busy += pf_dur;
-            psteps++;
-            __syncwarp();
-            // digest + trace record, batch order
             uint64_t h = mix64((uint64_t)t ^ 0xA5A5A5A5A5A5A5A5ULL);
-            if (T.buf && lane == 0) { T.put(T.used, SLOSIM_EV_PREFILL_DONE); T.put(T.used + 1, t); T.put(T.used + 2, pf_dur); T.put(T.used + 3, pf_k); }
+            if (T.buf && lane == 0) {
+                T.put(T.used, SLOSIM_EV_PREFILL_DONE); T.put(T.used + 1, t); T.put(T.used + 2, pf_dur); T.put(T.used + 3, pf_k);
+            }
             T.used += 4;
+            int64_t tw_transfers = T.used + pf_k;  // delay-0 TransferDone records follow the batch list
+            int ncomp = 0, n0 = 0;
             for (int base = 0; base < pf_k; base += 32) {
                 int e = base + lane;
+                bool v = e < pf_k;
+                int64_t take = 0;
+                int32_t pos = 0, inp = 0;
+                bool comp = false;
                 uint64_t word = 0;
-                if (e < pf_k) {
-                    word = ((uint64_t)(uint32_t)w.q_pos[w.pf_qidx[e]] << 32) | (uint32_t)w.pf_take[e];
+                if (v) {
+                    int qi = pf_qidx[e];
+                    take = pf_take[e];
+                    int32_t rem = q_rem[qi] - (int32_t)take;
+                    q_rem[qi] = rem;
+                    pos = q_pos[qi];
+                    inp = q_inp[qi];
+                    comp = rem == 0;
+                    word = ((uint64_t)(uint32_t)pos << 32) | (uint32_t)take;
                     T.put(T.used + e, (int64_t)word);
                 }
+                tot += take;
+                // digest, batch order
                 int lim = pf_k - base < 32 ? pf_k - base : 32;
                 for (int j = 0; j < lim; j++) h = mix64(h ^ __shfl_sync(FULLMASK, word, j));
-            }
-            T.used += pf_k;
-            h = mix64(h ^ (uint64_t)pf_dur);
-            D = mix64(D ^ h);
-            // completed requests leave the queue and start their KV transfer
-            int ncomp = 0;
-            for (int base = 0; base < pf_k; base += 32) {
-                int e = base + lane;
-                bool comp = false;
-                int32_t pos = 0, inp = 0;
-                if (e < pf_k) {
-                    int qi = w.pf_qidx[e];
-                    comp = w.q_rem[qi] == 0;
-                    pos = w.q_pos[qi];
-                    inp = w.q_inp[qi];
-                }
-                int64_t delay = comp ? I.transfer_base_us + rint_i64(xmul((double)inp, I.transfer_per_token_us)) : 0;
+                // completed requests leave the queue and start their KV transfer, batch order
+                int64_t delay = comp ? I->transfer_base_us + rint_i64(xmul((double)inp, I->transfer_per_token_us)) : 0;
                 unsigned cm = __ballot_sync(FULLMASK, comp);
+                unsigned zm = __ballot_sync(FULLMASK, comp && delay == 0);
+                if (T.buf && comp && delay == 0) {
+                    int64_t o = tw_transfers + 3 * (n0 + __popc(zm & lanemask_lt(lane)));
+                    T.put(o, SLOSIM_EV_TRANSFER_DONE); T.put(o + 1, t); T.put(o + 2, pos);
+                }
+                n0 += __popc(zm);
                 ncomp += __popc(cm);
-                if (rows && comp) R.t_prefill_finish[I.row_offset + pos] = t;
+                if (rows && comp) B->rows.t_prefill_finish[row0 + pos] = t;
                 while (cm) {
                     int j = __ffs((int)cm) - 1;
                     cm &= cm - 1;
@@ -622,17 +593,22 @@ __device__ void simulate(const Ctx& cx, int64_t ii, const WS& w, int lane) {
                     int64_t jdel = __shfl_sync(FULLMASK, delay, j);
                     if (jdel == 0) {
                         pending_insert(w, ph, pt, t, Tidr[jpos], t, jpos, lane);
-                        if (T.buf && lane == 0) { T.put(T.used, SLOSIM_EV_TRANSFER_DONE); T.put(T.used + 1, t); T.put(T.used + 2, jpos); }
-                        T.used += 3;
                     } else {
-                        if (lane == 0) { w.tr_t[trn] = t + jdel; w.tr_tpf[trn] = t; w.tr_pos[trn] = jpos; }
+                        if (lane == 0) { w.i64(TR_T)[trn] = t + jdel; w.i64(TR_TPF)[trn] = t; w.i32(TR_POS)[trn] = jpos; }
                         trn++;
                         tr_min = t + jdel < tr_min ? t + jdel : tr_min;
                     }
                 }
             }
+            T.used += pf_k + 3 * n0;
+            tot = wsum64(tot);
+            est_tok += tot;
+            est_busy += pf_dur;
+            psteps++;
+            h = mix64(h ^ (uint64_t)pf_dur);
+            D = mix64(D ^ h);
             __syncwarp();
-            if (I.prefill_policy == SLOSIM_PREFILL_FCFS) {
+            if (ppol == SLOSIM_PREFILL_FCFS) {
                 qh += ncomp;  // FCFS completes a prefix of the queue
             } else if (ncomp) {
                 int o = qh;
@@ -641,13 +617,13 @@ __device__ void simulate(const Ctx& cx, int64_t ii, const WS& w, int lane) {
                     bool v = qi < qt;
                     int32_t pos = 0, rem = 0, full = 0, inp = 0;
                     int64_t a = 0;
-                    if (v) { pos = w.q_pos[qi]; rem = w.q_rem[qi]; full = w.q_full[qi]; inp = w.q_inp[qi]; a = w.q_arr[qi]; }
+                    if (v) { pos = q_pos[qi]; rem = q_rem[qi]; full = q_full[qi]; inp = q_inp[qi]; a = q_arr[qi]; }
                     bool keep = v && rem > 0;
                     unsigned km = __ballot_sync(FULLMASK, keep);
                     __syncwarp();
                     if (keep) {
-                        int d = o + __popc(km & ((1u << lane) - 1u));
-                        w.q_pos[d] = pos; w.q_rem[d] = rem; w.q_full[d] = full; w.q_inp[d] = inp; w.q_arr[d] = a;
+                        int d = o + __popc(km & lanemask_lt(lane));
+                        q_pos[d] = pos; q_rem[d] = rem; q_full[d] = full; q_inp[d] = inp; q_arr[d] = a;
                     }
                     o += __popc(km);
                     __syncwarp();
@@ -659,22 +635,30 @@ __device__ void simulate(const Ctx& cx, int64_t ii, const WS& w, int lane) {
 
         // ---- decode step completion (engine.py:394-413)
         if (dc_end == t) {
+            int32_t* a_pos = w.i32(A_POS);
+            int32_t* a_seq = w.i32(A_SEQ);
+            int32_t* a_idr = w.i32(A_IDR);
+            int32_t* a_out = w.i32(A_OUT);
+            int32_t* a_inp = w.i32(A_INP);
+            int32_t* a_miss = w.i32(A_MISS);
+            int32_t* a_flag = w.i32(A_FLAG);
+            int64_t* a_tf = w.i64(A_TFIRST);
+            double* tps_buf = w.f64(TPS);
             uint64_t s = 0;
-            int64_t kv_rel = 0;
+            int64_t kv_rel = 0, mx = 0, miss_sum = 0;
             int o = 0;
             int64_t tw0 = T.used + 5;
             int nmem = 0;
             for (int base = 0; base < an; base += 32) {
                 int i = base + lane;
                 bool v = i < an;
-                int32_t flag = v ? w.a_flag[i] : 0;
-                bool inb = v && (flag & 1);
-                int32_t pos = 0, seq = 0, idr = 0, outl = 0, inp = 0, miss = 0;
+                int32_t flag = 0, pos = 0, seq = 0, idr = 0, outl = 0, inp = 0, miss = 0;
                 int64_t tf = 0;
                 if (v) {
-                    pos = w.a_pos[i]; seq = w.a_seq[i]; idr = w.a_idr[i]; outl = w.a_out[i]; inp = w.a_inp[i];
-                    miss = w.a_miss[i]; tf = w.a_tfirst[i];
+                    flag = a_flag[i]; pos = a_pos[i]; seq = a_seq[i]; idr = a_idr[i]; outl = a_out[i]; inp = a_inp[i];
+                    miss = a_miss[i]; tf = a_tf[i];
                 }
+                bool inb = v && (dc_prefix >= 0 ? i < dc_prefix : (flag & 1));
                 bool retire = false, tpm = false;
                 double tps = 0.0;
                 if (inb) {
@@ -692,44 +676,49 @@ __device__ void simulate(const Ctx& cx, int64_t ii, const WS& w, int lane) {
                         kv_rel += (int64_t)inp + outl;
                         if (rows) {
                             bool ttm = (flag & 2) != 0;
-                            int64_t g = I.row_offset + pos;
-                            R.mean_tpot_us[g] = tpot;
-                            R.decode_tps[g] = tps;
-                            R.met_flags[g] = (uint8_t)((ttm ? 1 : 0) | (tpm ? 2 : 0) | ((ttm && tpm) ? 4 : 0));
-                            R.deadline_misses[g] = miss;
-                            R.t_last_token[g] = t;
+                            int64_t g = row0 + pos;
+                            B->rows.mean_tpot_us[g] = tpot;
+                            B->rows.decode_tps[g] = tps;
+                            B->rows.met_flags[g] = (uint8_t)((ttm ? 1 : 0) | (tpm ? 2 : 0) | ((ttm && tpm) ? 4 : 0));
+                            B->rows.deadline_misses[g] = miss;
+                            B->rows.t_last_token[g] = t;
                         }
                     }
                 }
                 unsigned rmask = __ballot_sync(FULLMASK, retire);
-                if (retire) w.tps[ntps + __popc(rmask & ((1u << lane) - 1u))] = tps;
-                misses += wsum64(retire ? (int64_t)miss : 0);
+                if (retire) {
+                    tps_buf[ntps + __popc(rmask & lanemask_lt(lane))] = tps;
+                    miss_sum += miss;
+                }
                 ntps += __popc(rmask);
                 c_tpot += __popc(__ballot_sync(FULLMASK, retire && tpm));
                 c_e2e += __popc(__ballot_sync(FULLMASK, retire && tpm && (flag & 2)));
                 finished += __popc(rmask);
-                // trace: members
-                unsigned bm = __ballot_sync(FULLMASK, inb);
-                if (inb) T.put(tw0 + nmem + __popc(bm & ((1u << lane) - 1u)), pos);
-                nmem += __popc(bm);
+                if (T.buf) {
+                    unsigned bm = __ballot_sync(FULLMASK, inb);
+                    if (inb) T.put(tw0 + nmem + __popc(bm & lanemask_lt(lane)), pos);
+                    nmem += __popc(bm);
+                }
                 // compact survivors (stable), clearing the in-batch bit
                 bool keep = v && !retire;
                 unsigned km = __ballot_sync(FULLMASK, keep);
                 __syncwarp();
                 if (keep) {
-                    int d = o + __popc(km & ((1u << lane) - 1u));
-                    w.a_pos[d] = pos; w.a_seq[d] = seq; w.a_idr[d] = idr; w.a_out[d] = outl; w.a_inp[d] = inp;
-                    w.a_miss[d] = miss; w.a_tfirst[d] = tf; w.a_flag[d] = flag & ~1;
+                    int d = o + __popc(km & lanemask_lt(lane));
+                    a_pos[d] = pos; a_seq[d] = seq; a_idr[d] = idr; a_out[d] = outl; a_inp[d] = inp;
+                    a_miss[d] = miss; a_tf[d] = tf; a_flag[d] = flag & ~1;
+                    mx = seq > mx ? seq : mx;
                 }
                 o += __popc(km);
                 __syncwarp();
             }
             an = o;
+            amax = wmax64(mx);
+            misses += wsum64(miss_sum);
             kv -= wsum64(kv_rel);
             s = wsumu64(s);
             if (use_lut) {
                 if (lane == 0) lut_update(L, dc_bsz, dc_max, dc_dur);
-                L.rowmask = __shfl_sync(FULLMASK, L.rowmask, 0);
                 __syncwarp();
             }
             dsteps++;
@@ -742,7 +731,7 @@ __device__ void simulate(const Ctx& cx, int64_t ii, const WS& w, int lane) {
                 T.put(T.used, SLOSIM_EV_DECODE_DONE); T.put(T.used + 1, t); T.put(T.used + 2, dc_dur);
                 T.put(T.used + 3, dc_bsz); T.put(T.used + 4, dc_max);
             }
-            T.used += 5 + nmem;
+            T.used += 5 + (T.buf ? nmem : 0);
             dc_end = SLOSIM_INF64;
         }
 
@@ -750,37 +739,36 @@ __device__ void simulate(const Ctx& cx, int64_t ii, const WS& w, int lane) {
         while (pt > ph) {
             int k = ph + lane;
             bool v = k < pt;
-            int32_t pos = v ? w.pd_pos[k] : 0;
+            int32_t pos = v ? w.i32(PD_POS)[k] : 0;
             int32_t outl = v ? Tout[pos] : 0, inp = v ? Tinp[pos] : 0;
             int64_t need = (int64_t)inp + outl;
             int64_t held = (v && outl > 1) ? need : 0;
             int64_t excl = wscan_incl64(held, lane) - held;
-            bool ok = v && kv + excl + need <= I.kv_capacity_tokens;
+            bool ok = v && kv + excl + need <= kv_cap;
             unsigned vm = __ballot_sync(FULLMASK, v);
             unsigned okm = __ballot_sync(FULLMASK, ok);
             unsigned fail = vm & ~okm;
             int cnt = fail ? __ffs((int)fail) - 1 : __popc(vm);
             bool adm = lane < cnt;
-            int64_t ttr = adm ? w.pd_ttr[k] : 0;
-            int64_t ttft = 0;
+            int64_t ttr = adm ? w.i64(PD_TTR)[k] : 0;
             bool ttm = false;
             if (adm) {
-                ttft = ttr - arrival_of(Tarr, fac, pos);
+                int64_t ttft = ttr - arrival_of(Tarr, fac, pos);
                 ttm = ttft <= ttft_slo;
                 if (T.buf) {
                     int64_t o2 = T.used + 4 * lane;
                     T.put(o2, SLOSIM_EV_ADMIT); T.put(o2 + 1, t); T.put(o2 + 2, pos); T.put(o2 + 3, ttr);
                 }
                 if (rows) {
-                    int64_t g = I.row_offset + pos;
-                    R.ttft_us[g] = ttft;
-                    R.t_first_token[g] = ttr;
+                    int64_t g = row0 + pos;
+                    B->rows.ttft_us[g] = ttft;
+                    B->rows.t_first_token[g] = ttr;
                     if (outl == 1) {
-                        R.mean_tpot_us[g] = 0.0;
-                        R.decode_tps[g] = __longlong_as_double(0x7ff8000000000000LL);
-                        R.met_flags[g] = (uint8_t)((ttm ? 1 : 0) | 2 | (ttm ? 4 : 0));
-                        R.deadline_misses[g] = 0;
-                        R.t_last_token[g] = ttr;
+                        B->rows.mean_tpot_us[g] = 0.0;
+                        B->rows.decode_tps[g] = __longlong_as_double(0x7ff8000000000000LL);
+                        B->rows.met_flags[g] = (uint8_t)((ttm ? 1 : 0) | 2 | (ttm ? 4 : 0));
+                        B->rows.deadline_misses[g] = 0;
+                        B->rows.t_last_token[g] = ttr;
                     }
                 }
             }
@@ -792,11 +780,13 @@ __device__ void simulate(const Ctx& cx, int64_t ii, const WS& w, int lane) {
             finished += __popc(one);
             unsigned dec = __ballot_sync(FULLMASK, adm && outl > 1);
             if (adm && outl > 1) {
-                int d = an + __popc(dec & ((1u << lane) - 1u));
-                w.a_pos[d] = pos; w.a_seq[d] = inp; w.a_idr[d] = w.pd_idr[k]; w.a_out[d] = outl; w.a_inp[d] = inp;
-                w.a_miss[d] = 0; w.a_tfirst[d] = ttr; w.a_flag[d] = ttm ? 2 : 0;
+                int d = an + __popc(dec & lanemask_lt(lane));
+                w.i32(A_POS)[d] = pos; w.i32(A_SEQ)[d] = inp; w.i32(A_IDR)[d] = w.i32(PD_IDR)[k];
+                w.i32(A_OUT)[d] = outl; w.i32(A_INP)[d] = inp; w.i32(A_MISS)[d] = 0; w.i64(A_TFIRST)[d] = ttr;
+                w.i32(A_FLAG)[d] = ttm ? 2 : 0;
             }
             an += __popc(dec);
+            amax = wmax64(adm && outl > 1 && inp > amax ? (int64_t)inp : amax);
             kv += wsum64(adm ? held : 0);
             ph += cnt;
             __syncwarp();
@@ -808,25 +798,27 @@ __device__ void simulate(const Ctx& cx, int64_t ii, const WS& w, int lane) {
             int qlen = qt - qh;
             v_pre += qlen;
             max_q = qlen > max_q ? qlen : max_q;
-            pf_k = prefill_select(I.prefill_policy, w, qh, qt, I.chunk_budget, t, est_tok, est_busy, ttft_slo,
-                                  w.pf_qidx, w.pf_take, lane);
+            pf_k = prefill_select(ppol, w, qh, qt, I->chunk_budget, t, est_tok, est_busy, ttft_slo, lane);
             if (pf_k > 0) {
                 // ground-truth duration: ordered sum of curve increments (engine.py:175-183)
+                const int32_t* pf_qidx = w.i32(PF_QIDX);
+                const int32_t* pf_take = w.i32(PF_TAKE);
+                const int n_curve = P->n_curve;
                 double total = 0.0;
                 int64_t ww = 0;
                 for (int base = 0; base < pf_k; base += 32) {
                     int e = base + lane;
                     double term = 0.0;
                     if (e < pf_k) {
-                        int qi = w.pf_qidx[e];
-                        int64_t take = w.pf_take[e];
-                        int64_t done = (int64_t)w.q_full[qi] - w.q_rem[qi];
+                        int qi = pf_qidx[e];
+                        int64_t take = pf_take[e];
+                        int64_t done = (int64_t)q_full[qi] - q_rem[qi];
                         term = xsub(curve_at(n_curve, P->curve_x, P->curve_y, done + take),
                                     curve_at(n_curve, P->curve_x, P->curve_y, done));
                         if (done == 0) {  // first time scheduled (engine.py:322)
-                            int64_t wt = t - w.q_arr[qi];
+                            int64_t wt = t - q_arr[qi];
                             ww = wt > ww ? wt : ww;
-                            if (rows) R.first_sched_us[I.row_offset + w.q_pos[qi]] = t;
+                            if (rows) B->rows.first_sched_us[row0 + q_pos[qi]] = t;
                         }
                     }
                     int lim = pf_k - base < 32 ? pf_k - base : 32;
@@ -844,40 +836,35 @@ __device__ void simulate(const Ctx& cx, int64_t ii, const WS& w, int lane) {
         if (dc_end == SLOSIM_INF64 && an > 0) {
             v_dec += an;
             max_a = an > max_a ? an : max_a;
-            int64_t mx = 0;
-            for (int i = lane; i < an; i += 32) mx = w.a_seq[i] > mx ? w.a_seq[i] : mx;
-            mx = wmax64(mx);
             int bsz = an;
-            int64_t bmax = mx;
-            if (I.decode_policy == SLOSIM_DECODE_KAIROS_SLACK) {
+            int64_t bmax = amax;
+            dc_prefix = an;
+            if (dpol == SLOSIM_DECODE_KAIROS_SLACK) {
                 // select_decode_batch decode_sched.py:60-111
-                double fallback = lut_lookup(L, an, mx);
+                const int32_t* a_seq = w.i32(A_SEQ);
+                const int32_t* a_inp = w.i32(A_INP);
+                const int64_t* a_tf = w.i64(A_TFIRST);
+                double fallback = lut_lookup(L, an, amax);
                 int64_t sl = SLOSIM_INF64;
                 for (int i = lane; i < an; i += 32) {
-                    int64_t ngen = (int64_t)w.a_seq[i] - w.a_inp[i];
-                    int64_t v = tpot_slo * (ngen + 1) - (t - w.a_tfirst[i]);
+                    int64_t ngen = (int64_t)a_seq[i] - a_inp[i];
+                    int64_t v = tpot_slo * (ngen + 1) - (t - a_tf[i]);
                     sl = v < sl ? v : sl;
                 }
                 sl = wmin64(sl);
                 double smin = xsub((double)sl, fallback);
-                decode_order(an, w.a_seq, w.a_idr, w.a_ord, lane);
+                decode_order(an, a_seq, w.i32(A_IDR), w.i32(A_ORD), lane);
                 double tcur;
                 int64_t ms;
-                int b = decode_scan(L, an, w.a_ord, w.a_seq, w.a_flag, smin, &tcur, &ms, nullptr, nullptr, nullptr,
-                                    nullptr, lane);
-                __syncwarp();
-                if (b > 0) { bsz = b; bmax = ms; }
-                else {
-                    for (int i = lane; i < an; i += 32) w.a_flag[i] |= 1;
-                }
-            } else {
-                // continuous_batching_select decode_sched.py:114-124
-                for (int i = lane; i < an; i += 32) w.a_flag[i] |= 1;
+                int b = decode_scan(L, an, w.i32(A_ORD), a_seq, w.i32(A_FLAG), smin, &tcur, &ms, nullptr, nullptr,
+                                    nullptr, nullptr, lane);
+                if (b > 0) { bsz = b; bmax = ms; dc_prefix = -1; }
             }
-            __syncwarp();
             b_dec += bsz;
             // _GroundTruth.decode_step_us engine.py:185-192
-            double val = frozen ? lut_lookup(FZ, bsz, bmax) : decode_formula(n_base, P->base_x, P->base_y, gamma, bsz, bmax);
+            double val = P->gt_frozen ? lut_lookup(cx.frozen_tab + pid, bsz, bmax)
+                                      : decode_formula(P->n_base, P->base_x, P->base_y, P->gamma, bsz, bmax);
+            double eps = P->noise_eps;
             if (eps > 0) val = xmul(val, pcg_uniform(rng, xsub(1.0, eps), xadd(1.0, eps)));
             int64_t d = rint_i64(val);
             dc_dur = d < 1 ? 1 : d;
@@ -893,16 +880,17 @@ __device__ void simulate(const Ctx& cx, int64_t ii, const WS& w, int lane) {
     if (ntps > 0) {
         int64_t r50 = (int64_t)ceil(xmul(50 / 100.0, (double)ntps));
         int64_t r90 = (int64_t)ceil(xmul(90 / 100.0, (double)ntps));
-        p50 = radix_select(w.tps, ntps, r50 < 1 ? 1 : r50, lane);
-        p90 = radix_select(w.tps, ntps, r90 < 1 ? 1 : r90, lane);
+        p50 = radix_select(w.f64(TPS), ntps, r50 < 1 ? 1 : r50, lane);
+        p90 = radix_select(w.f64(TPS), ntps, r90 < 1 ? 1 : r90, lane);
     }
     if ((B->flags & SLOSIM_F_EXPORT_LUT) && B->lut_out_sums) {
-        const int FR = SLOSIM_MAX_BSZ_BUCKETS * SLOSIM_MAX_SEQ_BUCKETS;
+        const int FR = LUT_CELLS;
+        const int nb = P->nb, ns = P->ns;
         for (int c = lane; c < FR; c += 32) {
             int i = c / SLOSIM_MAX_SEQ_BUCKETS, j = c % SLOSIM_MAX_SEQ_BUCKETS;
             bool in = i < nb && j < ns;
-            B->lut_out_sums[ii * FR + c] = in ? w.l_sum[i * ns + j] : 0.0;
-            B->lut_out_counts[ii * FR + c] = in ? w.l_cnt[i * ns + j] : 0;
+            B->lut_out_sums[ii * FR + c] = in ? L->sum[i * ns + j] : 0.0;
+            B->lut_out_counts[ii * FR + c] = in ? L->cnt[i * ns + j] : 0;
         }
     }
     if (T.buf && lane == 0 && T.used + 2 <= T.cap) { T.buf[T.used] = SLOSIM_EV_END; T.buf[T.used + 1] = T.used + 2; }
@@ -920,15 +908,19 @@ __device__ void simulate(const Ctx& cx, int64_t ii, const WS& w, int lane) {
         s.t_end_us = t_end;
         s.est_tokens = est_tok; s.est_busy_us = est_busy;
         s.max_queue = max_q; s.max_active = max_a;
-        *out = s;
+        B->summaries[ii] = s;
     }
 }
 
-__global__ void __launch_bounds__(128) sim_kernel(const __grid_constant__ Ctx cx, char* ws_base, size_t ws_stride,
-                                                  int64_t cap, unsigned long long* work) {
+#ifndef SLOSIM_MIN_BLOCKS
+#define SLOSIM_MIN_BLOCKS 3
+#endif
+
+__global__ void __launch_bounds__(128, SLOSIM_MIN_BLOCKS)
+    sim_kernel(const __grid_constant__ Ctx cx, char* ws_base, size_t ws_stride, int64_t cap, unsigned long long* work) {
     const int lane = threadIdx.x & 31;
     const int64_t gw = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-    WS w = carve_ws(ws_base + (size_t)gw * ws_stride, cap);
+    WS w = make_ws(ws_base + (size_t)gw * ws_stride, cap);
     const int64_t N = cx.B.n_instances;
     for (;;) {
         unsigned long long ii = 0;

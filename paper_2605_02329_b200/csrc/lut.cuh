@@ -1,28 +1,40 @@
-// lut.cuh — DecodeStepLUT (costmodel.py:61-227) and the decode/prefill cost
-// formulas of the ground truth, as device code.
+// lut.cuh — DecodeStepLUT (costmodel.py:61-227) and the ground-truth cost
+// formulas (costmodel.py:32-58, engine.py:161-192) as device code.
 //
-// Layout: a compact [nb][ns] grid of f64 sums, f64 means, f64 slopes (np.interp
-// slope from each populated column to the next populated column of the same
-// row, costmodel.py:153-155 -> numpy arr_interp) and i32 counts, plus a u64
-// populated-column mask per row and a u32 populated-row mask.  Means and
-// slopes are recomputed for the touched cells at each update (one division per
-// affected value), so a lookup costs at most one division (the across-row
-// Python-form interpolation, costmodel.py:183-187).
+// One LUT is one LutMem block (reached through a single pointer, so it costs
+// two registers): compact [nb][ns] grids of f64 sums, means and np.interp
+// slopes (slope from each populated column to the next populated column of
+// its row), i32 counts, a u64 populated-column mask per row, a populated-row
+// mask, copies of the bucket arrays and two direct-index tables that replace
+// the bisections of the reference (bisect_left over bsz for b <= 256 and a
+// 256-entry coarse table over seq_len refined by <= a couple of steps).
+//
+// Fast path: once every cell is populated (true from the start for
+// synthesized profiles with prior_weight > 0, and forever after because
+// counts only grow) a lookup is   row selection(bsz) x column selection(seq)
+// -> slope*dx + mean per row, plus one division for the across-row Python-form
+// interpolation.  The column selection of a candidate is computed once per
+// decode step and reused across the greedy scan's rounds.
 #pragma once
 #include "numerics.cuh"
 
 namespace slosim {
 
-struct DLut {
-    int nb, ns;
-    const int32_t* bb;  // bsz buckets [nb]
-    const int32_t* sb;  // seq buckets [ns]
-    double* sum;        // [nb*ns]
-    double* mean;       // [nb*ns]
-    double* slope;      // [nb*ns]
-    int32_t* cnt;       // [nb*ns]
-    uint64_t* colmask;  // [nb]
+#define LUT_CELLS (SLOSIM_MAX_BSZ_BUCKETS * SLOSIM_MAX_SEQ_BUCKETS)
+
+struct LutMem {
+    double sum[LUT_CELLS];
+    double mean[LUT_CELLS];
+    double slope[LUT_CELLS];
+    int32_t cnt[LUT_CELLS];
+    uint64_t colmask[SLOSIM_MAX_BSZ_BUCKETS];
+    int32_t bb[SLOSIM_MAX_BSZ_BUCKETS];
+    int32_t sb[SLOSIM_MAX_SEQ_BUCKETS];
+    int32_t nb, ns, sshift, full;
     uint32_t rowmask;
+    int32_t populated;
+    uint8_t bidx[264];  // bidx[b] = bisect_left(bb, b), b <= 256
+    uint8_t sidx[264];  // sidx[q] = bisect_left(sb, q << sshift), q <= 256
 };
 
 __device__ __forceinline__ int bisect_left(const int32_t* a, int n, int64_t x) {
@@ -40,78 +52,186 @@ __device__ __forceinline__ int bucket_index(const int32_t* a, int n, int64_t x) 
     return i < n - 1 ? i : n - 1;
 }
 
+__device__ __forceinline__ int lut_bidx(const LutMem* L, int64_t b) {
+    return (b >= 0 && b <= 256) ? (int)L->bidx[b] : bisect_left(L->bb, L->nb, b);
+}
+
+__device__ __forceinline__ int lut_sidx(const LutMem* L, int64_t s) {
+    int64_t q = s >> L->sshift;
+    if (q < 0 || q > 256) return bisect_left(L->sb, L->ns, s);
+    int j = L->sidx[q];
+    while (j < L->ns && (int64_t)L->sb[j] < s) j++;
+    return j;
+}
+
 __device__ __forceinline__ uint64_t low_mask64(int j) { return j >= 64 ? ~0ULL : ((1ULL << j) - 1ULL); }
 
-// Recompute the np.interp slope leaving column j of row i (to the next populated column).
-__device__ __forceinline__ void lut_fix_slope(DLut& L, int i, int j) {
-    uint64_t m = L.colmask[i] & ~low_mask64(j + 1);
-    if (m == 0) return;
+// Recompute the slope leaving column j of row i (to the next populated column).
+__device__ __forceinline__ void lut_fix_slope(LutMem* L, int i, int j) {
+    uint64_t m = L->colmask[i] & ~low_mask64(j + 1);
+    int c = i * L->ns;
+    if (m == 0) { L->slope[c + j] = 0.0; return; }
     int nx = __ffsll((long long)m) - 1;
-    int c = i * L.ns;
-    L.slope[c + j] = xdiv(xsub(L.mean[c + nx], L.mean[c + j]), xsub((double)L.sb[nx], (double)L.sb[j]));
+    L->slope[c + j] = xdiv(xsub(L->mean[c + nx], L->mean[c + j]), xsub((double)L->sb[nx], (double)L->sb[j]));
 }
 
 // Single-thread (re)build of row i's means, mask and slopes.
-__device__ void lut_build_row(DLut& L, int i) {
+__device__ void lut_build_row(LutMem* L, int i) {
     uint64_t m = 0;
-    int c = i * L.ns;
-    for (int j = 0; j < L.ns; j++) {
-        if (L.cnt[c + j] > 0) {
+    int c = i * L->ns;
+    for (int j = 0; j < L->ns; j++) {
+        if (L->cnt[c + j] > 0) {
             m |= 1ULL << j;
-            L.mean[c + j] = xdiv(L.sum[c + j], (double)L.cnt[c + j]);
+            L->mean[c + j] = xdiv(L->sum[c + j], (double)L->cnt[c + j]);
+        } else {
+            L->mean[c + j] = 0.0;
         }
+        L->slope[c + j] = 0.0;
     }
-    L.colmask[i] = m;
-    if (m) L.rowmask |= 1u << i; else L.rowmask &= ~(1u << i);
-    for (int j = 0; j < L.ns; j++)
+    L->colmask[i] = m;
+    for (int j = 0; j < L->ns; j++)
         if ((m >> j) & 1ULL) lut_fix_slope(L, i, j);
 }
 
+// Warp-cooperative build of a LutMem from a 16x64-framed (sums, counts) pair.
+__device__ void lut_build(LutMem* L, int nb, int ns, const int32_t* bb, const int32_t* sb, const double* fsums,
+                          const int32_t* fcounts, int lane) {
+    for (int c = lane; c < nb * ns; c += 32) {
+        int i = c / ns, j = c % ns;
+        L->sum[c] = fsums[i * SLOSIM_MAX_SEQ_BUCKETS + j];
+        L->cnt[c] = fcounts[i * SLOSIM_MAX_SEQ_BUCKETS + j];
+    }
+    if (lane < nb) L->bb[lane] = bb[lane];
+    for (int j = lane; j < ns; j += 32) L->sb[j] = sb[j];
+    int sshift = 0;
+    while (((int64_t)256 << sshift) < (int64_t)sb[ns - 1]) sshift++;
+    if (lane == 0) { L->nb = nb; L->ns = ns; L->sshift = sshift; }  // read by lut_build_row below
+    __syncwarp();
+    for (int q = lane; q < 264; q += 32) {
+        L->bidx[q] = (uint8_t)bisect_left(bb, nb, q);
+        L->sidx[q] = (uint8_t)bisect_left(sb, ns, (int64_t)q << sshift);
+    }
+    if (lane < nb) lut_build_row(L, lane);
+    __syncwarp();
+    bool pop = lane < nb && L->colmask[lane] != 0;
+    uint32_t rm = __ballot_sync(0xffffffffu, pop);
+    int cells = 0;
+    for (int c = lane; c < nb * ns; c += 32) cells += L->cnt[c] > 0;
+#pragma unroll
+    for (int o = 16; o; o >>= 1) cells += __shfl_xor_sync(0xffffffffu, cells, o);
+    if (lane == 0) {
+        L->rowmask = rm;
+        L->populated = cells;
+        L->full = cells == nb * ns;
+    }
+    __syncwarp();
+}
+
+// Copy of a built LutMem (only the live part of the frame).
+__device__ void lut_copy(LutMem* dst, const LutMem* src, int lane) {
+    int K = src->nb * src->ns;
+    for (int c = lane; c < K; c += 32) {
+        dst->sum[c] = src->sum[c]; dst->mean[c] = src->mean[c]; dst->slope[c] = src->slope[c]; dst->cnt[c] = src->cnt[c];
+    }
+    if (lane < src->nb) { dst->colmask[lane] = src->colmask[lane]; dst->bb[lane] = src->bb[lane]; }
+    for (int j = lane; j < src->ns; j += 32) dst->sb[j] = src->sb[j];
+    const uint32_t* s32 = (const uint32_t*)src->bidx;
+    uint32_t* d32 = (uint32_t*)dst->bidx;
+    for (int k = lane; k < 2 * 264 / 4; k += 32) d32[k] = s32[k];
+    if (lane == 0) {
+        dst->nb = src->nb; dst->ns = src->ns; dst->sshift = src->sshift; dst->full = src->full;
+        dst->rowmask = src->rowmask; dst->populated = src->populated;
+    }
+    __syncwarp();
+}
+
+// ---- full-grid fast path ----------------------------------------------------
+struct ColSel { int c; double dx; };   // value of a row = slope[row][c]*dx + mean[row][c]
+struct RowSel { int r1, r2; int64_t num, den; };  // r2 < 0: single row r1
+
+// np.interp column selection (numpy arr_interp) for a fully populated row.
+__device__ __forceinline__ ColSel lut_col(const LutMem* L, int64_t seq) {
+    int ns = L->ns;
+    if (seq <= (int64_t)L->sb[0]) return ColSel{0, 0.0};
+    if (seq >= (int64_t)L->sb[ns - 1]) return ColSel{ns - 1, 0.0};
+    int j0 = lut_sidx(L, seq);
+    if ((int64_t)L->sb[j0] == seq) return ColSel{j0, 0.0};
+    return ColSel{j0 - 1, xsub((double)seq, (double)L->sb[j0 - 1])};
+}
+
+// Row selection of lookup() (costmodel.py:175-187) when every row is populated.
+__device__ __forceinline__ RowSel lut_rows(const LutMem* L, int64_t bsz) {
+    int i = lut_bidx(L, bsz);
+    if (i == 0) return RowSel{0, -1, 0, 1};
+    if (i == L->nb) return RowSel{L->nb - 1, -1, 0, 1};
+    if ((int64_t)L->bb[i] == bsz) return RowSel{i, -1, 0, 1};
+    return RowSel{i - 1, i, bsz - L->bb[i - 1], (int64_t)L->bb[i] - L->bb[i - 1]};
+}
+
+__device__ __forceinline__ double lut_eval(const LutMem* L, const RowSel& rs, const ColSel& cs) {
+    int ns = L->ns;
+    int k1 = rs.r1 * ns + cs.c;
+    double v1 = xadd(xmul(L->slope[k1], cs.dx), L->mean[k1]);
+    if (rs.r2 < 0) return v1;
+    int k2 = rs.r2 * ns + cs.c;
+    double v2 = xadd(xmul(L->slope[k2], cs.dx), L->mean[k2]);
+    // v_lo + (v_hi - v_lo) * (bsz - b_lo) / (b_hi - b_lo)
+    return xadd(v1, xdiv(xmul(xsub(v2, v1), (double)rs.num), (double)rs.den));
+}
+
+// ---- general path -----------------------------------------------------------
 // np.interp(seq, xs, ys) over the populated columns of row r; j0 = bisect_left(sb, seq).
-__device__ __forceinline__ double lut_row_eval(const DLut& L, int r, int64_t seq, int j0) {
-    uint64_t m = L.colmask[r];
-    int c = r * L.ns;
+__device__ __forceinline__ double lut_row_eval(const LutMem* L, int r, int64_t seq, int j0) {
+    uint64_t m = L->colmask[r];
+    int c = r * L->ns;
     int first = __ffsll((long long)m) - 1;
     int last = 63 - __clzll((long long)m);
-    if (first == last) return L.mean[c + first];
-    if (seq <= (int64_t)L.sb[first]) return L.mean[c + first];
-    if (seq >= (int64_t)L.sb[last]) return L.mean[c + last];
-    if (j0 < L.ns && (int64_t)L.sb[j0] == seq && ((m >> j0) & 1ULL)) return L.mean[c + j0];
+    if (first == last) return L->mean[c + first];
+    if (seq <= (int64_t)L->sb[first]) return L->mean[c + first];
+    if (seq >= (int64_t)L->sb[last]) return L->mean[c + last];
+    if (j0 < L->ns && (int64_t)L->sb[j0] == seq && ((m >> j0) & 1ULL)) return L->mean[c + j0];
     int jp = 63 - __clzll((long long)(m & low_mask64(j0)));
-    // numpy: slope*(x - xp[j]) + fp[j]
-    return xadd(xmul(L.slope[c + jp], xsub((double)seq, (double)L.sb[jp])), L.mean[c + jp]);
+    return xadd(xmul(L->slope[c + jp], xsub((double)seq, (double)L->sb[jp])), L->mean[c + jp]);
 }
 
 // DecodeStepLUT.lookup costmodel.py:157-187 (bsz, seq >= 1; LUT non-empty).
-__device__ __forceinline__ double lut_lookup(const DLut& L, int64_t bsz, int64_t seq) {
-    int i = bisect_left(L.bb, L.nb, bsz);
-    int j0 = bisect_left(L.sb, L.ns, seq);
-    if (i < L.nb && (int64_t)L.bb[i] == bsz && j0 < L.ns && (int64_t)L.sb[j0] == seq && L.cnt[i * L.ns + j0] > 0)
-        return L.mean[i * L.ns + j0];
-    uint32_t below = L.rowmask & ((1u << i) - 1u);
-    uint32_t above = i >= 32 ? 0u : (L.rowmask >> i);
-    if (below == 0) return lut_row_eval(L, __ffs((int)L.rowmask) - 1, seq, j0);
-    if (above == 0) return lut_row_eval(L, 31 - __clz((int)L.rowmask), seq, j0);
+__device__ __forceinline__ double lut_lookup(const LutMem* L, int64_t bsz, int64_t seq) {
+    if (L->full) return lut_eval(L, lut_rows(L, bsz), lut_col(L, seq));
+    int i = lut_bidx(L, bsz);
+    int j0 = lut_sidx(L, seq);
+    int nb = L->nb, ns = L->ns;
+    if (i < nb && (int64_t)L->bb[i] == bsz && j0 < ns && (int64_t)L->sb[j0] == seq && L->cnt[i * ns + j0] > 0)
+        return L->mean[i * ns + j0];
+    uint32_t rowmask = L->rowmask;
+    uint32_t below = rowmask & ((1u << i) - 1u);
+    uint32_t above = i >= 32 ? 0u : (rowmask >> i);
+    if (below == 0) return lut_row_eval(L, __ffs((int)rowmask) - 1, seq, j0);
+    if (above == 0) return lut_row_eval(L, 31 - __clz((int)rowmask), seq, j0);
     int rhi = i + __ffs((int)above) - 1;
-    if ((int64_t)L.bb[rhi] == bsz) return lut_row_eval(L, rhi, seq, j0);
+    if ((int64_t)L->bb[rhi] == bsz) return lut_row_eval(L, rhi, seq, j0);
     int rlo = 31 - __clz((int)below);
     double vlo = lut_row_eval(L, rlo, seq, j0);
     double vhi = lut_row_eval(L, rhi, seq, j0);
-    // v_lo + (v_hi - v_lo) * (bsz - b_lo) / (b_hi - b_lo)
-    return xadd(vlo, xdiv(xmul(xsub(vhi, vlo), (double)(bsz - L.bb[rlo])), (double)(L.bb[rhi] - L.bb[rlo])));
+    return xadd(vlo, xdiv(xmul(xsub(vhi, vlo), (double)(bsz - L->bb[rlo])), (double)(L->bb[rhi] - L->bb[rlo])));
 }
 
-// DecodeStepLUT.update costmodel.py:118-128 (single thread).
-__device__ void lut_update(DLut& L, int64_t bsz, int64_t max_seq, int64_t obs) {
-    int i = bucket_index(L.bb, L.nb, bsz), j = bucket_index(L.sb, L.ns, max_seq);
-    int c = i * L.ns + j;
-    bool fresh = L.cnt[c] == 0;
-    L.sum[c] = xadd(L.sum[c], (double)obs);
-    L.cnt[c] += 1;
-    if (fresh) { lut_build_row(L, i); return; }
-    L.mean[c] = xdiv(L.sum[c], (double)L.cnt[c]);
+// DecodeStepLUT.update costmodel.py:118-128 (single thread; caller syncs the warp).
+__device__ void lut_update(LutMem* L, int64_t bsz, int64_t max_seq, int64_t obs) {
+    int i = bucket_index(L->bb, L->nb, bsz), j = bucket_index(L->sb, L->ns, max_seq);
+    int c = i * L->ns + j;
+    bool fresh = L->cnt[c] == 0;
+    L->sum[c] = xadd(L->sum[c], (double)obs);
+    L->cnt[c] += 1;
+    if (fresh) {
+        lut_build_row(L, i);
+        L->rowmask |= 1u << i;
+        L->populated += 1;
+        L->full = L->populated == L->nb * L->ns;
+        return;
+    }
+    L->mean[c] = xdiv(L->sum[c], (double)L->cnt[c]);
     lut_fix_slope(L, i, j);
-    uint64_t prev = L.colmask[i] & low_mask64(j);
+    uint64_t prev = L->colmask[i] & low_mask64(j);
     if (prev) lut_fix_slope(L, i, 63 - __clzll((long long)prev));
 }
 

@@ -59,16 +59,27 @@ __device__ __forceinline__ double idiv_prod(int64_t a, int64_t b, int64_t c) {
     return idiv128(p, (__int128)c);
 }
 
-// ceil(tokens * busy / total), exact (costmodel.py:267-268).
+// ceil(tokens * busy / total), exact (costmodel.py:267-268).  The quotient is
+// estimated with one f64 division and corrected with the exact integer
+// remainder (|error| <= 1 unit for the operand ranges of the engine); a
+// 128-bit long division handles products >= 2^62.
+__device__ __noinline__ int64_t ceil_muldiv_slow(int64_t tokens, int64_t busy, int64_t total) {
+    unsigned __int128 num = (unsigned __int128)(uint64_t)tokens * (uint64_t)busy;
+    return (int64_t)((num + (unsigned __int128)total - 1) / (unsigned __int128)total);
+}
+
 __device__ __forceinline__ int64_t ceil_muldiv(int64_t tokens, int64_t busy, int64_t total) {
     if (tokens == 0) return 0;
     uint64_t hi = __umul64hi((uint64_t)tokens, (uint64_t)busy);
-    uint64_t lo = (uint64_t)tokens * (uint64_t)busy;
-    if (hi == 0 && lo <= (uint64_t)0x7fffffffffffffffULL - (uint64_t)total) {
-        return (int64_t)((lo + (uint64_t)total - 1) / (uint64_t)total);
-    }
-    unsigned __int128 num = ((unsigned __int128)hi << 64) | lo;
-    return (int64_t)((num + (unsigned __int128)total - 1) / (unsigned __int128)total);
+    uint64_t n = (uint64_t)tokens * (uint64_t)busy;
+    if (hi != 0 || n >= (1ULL << 62)) return ceil_muldiv_slow(tokens, busy, total);
+    uint64_t d = (uint64_t)total;
+    uint64_t q = (uint64_t)__ddiv_rz((double)n, (double)d);
+    int64_t r = (int64_t)(n - q * d);
+    int guard = 0;
+    while (r < 0) { q--; r += (int64_t)d; if (++guard > 4) return ceil_muldiv_slow(tokens, busy, total); }
+    while (r >= (int64_t)d) { q++; r -= (int64_t)d; if (++guard > 4) return ceil_muldiv_slow(tokens, busy, total); }
+    return (int64_t)(q + (r != 0));
 }
 
 // splitmix64 finalizer used by the decision digest.
