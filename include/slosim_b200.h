@@ -237,10 +237,12 @@ int slosim_prefill_batch_us(int32_t n_curve, const int64_t* curve_x, const int64
 
 /* ----------------------------------------------------------- metrics (A18-A19)
  * Replaces request_metrics + aggregate (metrics.py:72-144) over explicit token
- * timestamps (CSR: offsets[n+1]); rows sorted by the caller. */
-int slosim_request_metrics(int64_t n, const int64_t* arrival, const int64_t* output_len,
-                           const int64_t* ts_offsets, const int64_t* ts, int64_t ttft_slo_us,
-                           int64_t tpot_slo_us, int64_t* ttft_us, double* mean_tpot, double* tps,
+ * timestamps (CSR: ts_offsets[n+1]).  Times are f64 so both the int-µs engine and
+ * float-time callers (tests/oracles.py:33-68) are reproduced exactly (integers
+ * below 2^53 convert exactly, so int/int true division is matched). */
+int slosim_request_metrics(int64_t n, const double* arrival, const int64_t* output_len,
+                           const int64_t* ts_offsets, const double* ts, int64_t ttft_slo_us,
+                           int64_t tpot_slo_us, double* ttft_us, double* mean_tpot, double* tps,
                            uint8_t* met_flags, int32_t* misses, double* agg /* [5]: att x3, p50, p90 */);
 
 /* K6 pre-collective step: hist[cell[k]][e2e_met of instance k] += 1 over a device

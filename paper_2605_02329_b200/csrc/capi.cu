@@ -353,26 +353,29 @@ __global__ void k_prefill_gt(int nc, const int64_t* cx, const int64_t* cy, int k
     *out = d < 1 ? 1 : d;
 }
 
-__global__ void k_request_metrics(int64_t n, const int64_t* arr, const int64_t* outl, const int64_t* off,
-                                  const int64_t* ts, int64_t ttft_slo, int64_t tpot_slo, int64_t* ttft, double* tpot,
+__global__ void k_request_metrics(int64_t n, const double* arr, const int64_t* outl, const int64_t* off,
+                                  const double* ts, int64_t ttft_slo, int64_t tpot_slo, double* ttft, double* tpot,
                                   double* tps, uint8_t* flags, int32_t* misses) {
     int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (k >= n) return;
-    const int64_t* tk = ts + off[k];
+    const double* tk = ts + off[k];
     int64_t m = off[k + 1] - off[k];
-    int64_t tf = tk[0];
-    int64_t v = tf - arr[k];
-    bool tm = v <= ttft_slo;
+    double tf = tk[0];
+    // ttft_metric metrics.py:30-35
+    double v = xsub(tf, arr[k]);
+    bool tm = v <= (double)ttft_slo;
     double tp = 0.0, tr = __longlong_as_double(0x7ff8000000000000LL);
     bool pm = true;
     if (outl[k] != 1) {
-        int64_t span = tk[m - 1] - tf;
-        tp = idiv(span, outl[k] - 1);
+        // tpot_metric :38-46, decode_throughput :49-54
+        double span = xsub(tk[m - 1], tf);
+        tp = xdiv(span, (double)(outl[k] - 1));
         pm = tp <= (double)tpot_slo;
-        tr = xdiv((double)(outl[k] - 1), xdiv((double)span, 1e6));
+        tr = xdiv((double)(outl[k] - 1), xdiv(span, 1e6));
     }
+    // deadline_misses :57-69: token j due at t_first + j * tpot
     int32_t mi = 0;
-    for (int64_t j = 1; j < m; j++) mi += tk[j] > tf + j * tpot_slo;
+    for (int64_t j = 1; j < m; j++) mi += tk[j] > xadd(tf, (double)(j * tpot_slo));
     ttft[k] = v; tpot[k] = tp; tps[k] = tr;
     flags[k] = (uint8_t)((tm ? 1 : 0) | (pm ? 2 : 0) | ((tm && pm) ? 4 : 0));
     misses[k] = mi;
@@ -672,9 +675,9 @@ extern "C" int slosim_prefill_batch_us(int32_t n_curve, const int64_t* cx, const
     return SLOSIM_OK;
 }
 
-extern "C" int slosim_request_metrics(int64_t n, const int64_t* arrival, const int64_t* output_len,
-                                      const int64_t* ts_offsets, const int64_t* ts, int64_t ttft_slo_us,
-                                      int64_t tpot_slo_us, int64_t* ttft_us, double* mean_tpot, double* tps,
+extern "C" int slosim_request_metrics(int64_t n, const double* arrival, const int64_t* output_len,
+                                      const int64_t* ts_offsets, const double* ts, int64_t ttft_slo_us,
+                                      int64_t tpot_slo_us, double* ttft_us, double* mean_tpot, double* tps,
                                       uint8_t* met_flags, int32_t* misses, double* agg) {
     if (n < 0) return SLOSIM_EINVAL;
     if (n == 0) {
@@ -686,11 +689,11 @@ extern "C" int slosim_request_metrics(int64_t n, const int64_t* arrival, const i
     std::lock_guard<std::mutex> lock(g_mu);
     CK(snap_reserve((size_t)n * 80 + (size_t)nts * 8 + 8192));
     Bump bp{(char*)g_snap.ptr};
-    int64_t* da = bp.take<int64_t>(n);
+    double* da = bp.take<double>(n);
     int64_t* dol = bp.take<int64_t>(n);
     int64_t* doff = bp.take<int64_t>(n + 1);
-    int64_t* dts = bp.take<int64_t>(nts);
-    int64_t* dtt = bp.take<int64_t>(n);
+    double* dts = bp.take<double>(nts);
+    double* dtt = bp.take<double>(n);
     double* dtp = bp.take<double>(n);
     double* dtr = bp.take<double>(n);
     uint8_t* dfl = bp.take<uint8_t>(n);

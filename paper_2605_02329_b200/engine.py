@@ -150,66 +150,83 @@ class Simulation:
         )
 
     def _restore(self, tr, packed, by_pos) -> None:
-        """Rebuild Python-side request state, events, LUT and estimator from device outputs."""
-        n = len(tr)
-        reqs_by_pos = [None] * n
-        orig_index = {}
-        for k, r in enumerate(self.requests):
-            reqs_by_pos[by_pos[r.id]] = r
-            orig_index[r.id] = k
-        R = packed.rows
-        recs = decode_trace(packed.trace_buf)
-        if int(packed.summaries[0]["status"]) & 0x100:
-            raise EngineError("event trace buffer overflow")
-        ngen = [0] * n
-        events = []
-        for rec in recs:
-            kind, t = rec[0], rec[1]
-            if kind == _abi.EV_ARRIVAL:
-                events.append({"t_us": t, "kind": "Arrival", "req": tr.id_of(rec[2]), "detail": {}})
-            elif kind == _abi.EV_TRANSFER_DONE:
-                events.append({"t_us": t, "kind": "TransferDone", "req": tr.id_of(rec[2]), "detail": {}})
-            elif kind == _abi.EV_ADMIT:
-                r = reqs_by_pos[rec[2]]
-                r.record_first_token(rec[3])
-                events.append({"t_us": t, "kind": "Admit", "req": r.id, "detail": {"first_token_us": rec[3]}})
-            elif kind == _abi.EV_PREFILL_DONE:
-                events.append({"t_us": t, "kind": "PrefillStepDone", "req": None,
-                               "detail": {"batch": [[tr.id_of(p), take] for p, take in rec[3]], "duration_us": rec[2]}})
-            elif kind == _abi.EV_DECODE_DONE:
-                mem = sorted(rec[5], key=lambda p: (int(tr.input_len[p]) + ngen[p], tr.id_of(p)))
-                for p in mem:
-                    reqs_by_pos[p].record_decode_token(t)
-                    ngen[p] += 1
-                events.append({"t_us": t, "kind": "DecodeStepDone", "req": None,
-                               "detail": {"batch": [tr.id_of(p) for p in mem], "bsz": rec[3], "max_seq": rec[4],
-                                          "duration_us": rec[2]}})
-        # arrivals at one instant are logged in workload order (engine.py:262-263)
-        i = 0
-        while i < len(events):
-            j = i
-            while (j < len(events) and events[j]["kind"] == "Arrival" and events[j]["t_us"] == events[i]["t_us"]):
-                j += 1
-            if j - i > 1:
-                events[i:j] = sorted(events[i:j], key=lambda e: orig_index[e["req"]])
-            i = max(j, i + 1)
-        for p in range(n):
-            r = reqs_by_pos[p]
-            r.prefill_done_tokens = r.input_len - r.prefix_hit_len
-            r.t_prefill_finish = int(R["t_prefill_finish"][p])
-            r.phase = Phase.FINISHED
+        events, lut, est = restore_state(self.requests, tr, packed, 0, self.lut.bsz_buckets, self.lut.seq_buckets)
         if self.events is not None:
             self.events = events
-        # final LUT and estimator (Simulation.lut / .estimator)
-        lut = DecodeStepLUT(self.lut.bsz_buckets, self.lut.seq_buckets)
+        self.lut = lut
+        self.estimator = est
+
+
+def restore_state(requests: list, tr, packed, inst: int, bsz_buckets, seq_buckets):
+    """Rebuild reference-side state of instance `inst` from device outputs.
+
+    Mutates `requests` (token timestamps, prefill progress, phase) and returns
+    (events, final DecodeStepLUT, final PrefillThroughputEstimator), the
+    reference's Simulation.events / .lut / .estimator (engine.py:234-257).
+    """
+    n = len(tr)
+    by_pos = {tr.id_of(p): p for p in range(n)}
+    reqs_by_pos = [None] * n
+    orig_index = {}
+    for k, r in enumerate(requests):
+        reqs_by_pos[by_pos[r.id]] = r
+        orig_index[r.id] = k
+    R = packed.rows
+    off = int(packed.instances[inst]["trace_buf_offset"])
+    words = int(packed.instances[inst]["trace_buf_words"])
+    if int(packed.summaries[inst]["status"]) & 0x100:
+        raise EngineError("event trace buffer overflow")
+    recs = decode_trace(packed.trace_buf[off:off + words])
+    row0 = int(packed.instances[inst]["row_offset"])
+    ngen = [0] * n
+    events = []
+    for rec in recs:
+        kind, t = rec[0], rec[1]
+        if kind == _abi.EV_ARRIVAL:
+            events.append({"t_us": t, "kind": "Arrival", "req": tr.id_of(rec[2]), "detail": {}})
+        elif kind == _abi.EV_TRANSFER_DONE:
+            events.append({"t_us": t, "kind": "TransferDone", "req": tr.id_of(rec[2]), "detail": {}})
+        elif kind == _abi.EV_ADMIT:
+            r = reqs_by_pos[rec[2]]
+            r.record_first_token(rec[3])
+            events.append({"t_us": t, "kind": "Admit", "req": r.id, "detail": {"first_token_us": rec[3]}})
+        elif kind == _abi.EV_PREFILL_DONE:
+            events.append({"t_us": t, "kind": "PrefillStepDone", "req": None,
+                           "detail": {"batch": [[tr.id_of(p), take] for p, take in rec[3]], "duration_us": rec[2]}})
+        elif kind == _abi.EV_DECODE_DONE:
+            # selection.batch order: ascending (seq_len, id) at step start (decode_sched.py:74)
+            mem = sorted(rec[5], key=lambda p: (int(tr.input_len[p]) + ngen[p], tr.id_of(p)))
+            for p in mem:
+                reqs_by_pos[p].record_decode_token(t)
+                ngen[p] += 1
+            events.append({"t_us": t, "kind": "DecodeStepDone", "req": None,
+                           "detail": {"batch": [tr.id_of(p) for p in mem], "bsz": rec[3], "max_seq": rec[4],
+                                      "duration_us": rec[2]}})
+    # arrivals at one instant are logged in workload order (engine.py:262-263)
+    i = 0
+    while i < len(events):
+        j = i
+        while j < len(events) and events[j]["kind"] == "Arrival" and events[j]["t_us"] == events[i]["t_us"]:
+            j += 1
+        if j - i > 1:
+            events[i:j] = sorted(events[i:j], key=lambda e: orig_index[e["req"]])
+        i = max(j, i + 1)
+    for p in range(n):
+        r = reqs_by_pos[p]
+        r.prefill_done_tokens = r.input_len - r.prefix_hit_len
+        if R is not None:
+            r.t_prefill_finish = int(R["t_prefill_finish"][row0 + p])
+        r.phase = Phase.FINISHED
+    lut = DecodeStepLUT(bsz_buckets, seq_buckets)
+    if packed.lut_out_sums is not None:
         nb, ns = len(lut.bsz_buckets), len(lut.seq_buckets)
-        fs = packed.lut_out_sums[0].reshape(_abi.MAX_B, _abi.MAX_S)
-        fc = packed.lut_out_counts[0].reshape(_abi.MAX_B, _abi.MAX_S)
+        fs = packed.lut_out_sums[inst].reshape(_abi.MAX_B, _abi.MAX_S)
+        fc = packed.lut_out_counts[inst].reshape(_abi.MAX_B, _abi.MAX_S)
         lut._sums[:, :] = fs[:nb, :ns]
         lut._counts[:, :] = fc[:nb, :ns]
-        self.lut = lut
-        s = packed.summaries[0]
-        self.estimator = PrefillThroughputEstimator(int(s["est_tokens"]), int(s["est_busy_us"]))
+    s = packed.summaries[inst]
+    est = PrefillThroughputEstimator(int(s["est_tokens"]), int(s["est_busy_us"]))
+    return events, lut, est
 
 
 def run(config: ClusterConfig, workload: list, *, collect_events: bool = False) -> MetricsReport:

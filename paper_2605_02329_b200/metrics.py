@@ -51,14 +51,14 @@ def _device_metrics(reqs: list, slo: SLOConfig):
     for r in reqs:
         if r.t_first_token is None:
             raise ValueError(f"{r.id}: no first token recorded")
-    arr = np.array([r.arrival_time for r in reqs], np.int64)
+    arr = np.array([r.arrival_time for r in reqs], np.float64)
     outl = np.array([r.output_len for r in reqs], np.int64)
     off = np.zeros(n + 1, np.int64)
     off[1:] = np.cumsum([len(r.token_timestamps) for r in reqs])
-    ts = np.array([t for r in reqs for t in r.token_timestamps], np.int64) if n else np.zeros(1, np.int64)
+    ts = np.array([t for r in reqs for t in r.token_timestamps], np.float64) if n else np.zeros(1, np.float64)
     if ts.size == 0:
-        ts = np.zeros(1, np.int64)
-    ttft = np.zeros(max(n, 1), np.int64)
+        ts = np.zeros(1, np.float64)
+    ttft = np.zeros(max(n, 1), np.float64)
     tpot = np.zeros(max(n, 1), np.float64)
     tps = np.zeros(max(n, 1), np.float64)
     flags = np.zeros(max(n, 1), np.uint8)
@@ -74,8 +74,9 @@ def _device_metrics(reqs: list, slo: SLOConfig):
 
 
 def _row(rid, ttft, tpot, tps, flags, miss) -> RequestMetrics:
+    ttft = float(ttft)
     return RequestMetrics(
-        id=rid, ttft_us=int(ttft), mean_tpot_us=float(tpot),
+        id=rid, ttft_us=int(ttft) if ttft.is_integer() else ttft, mean_tpot_us=float(tpot),
         decode_tps=None if math.isnan(tps) else float(tps),
         ttft_met=bool(flags & 1), tpot_met=bool(flags & 2), e2e_met=bool(flags & 4),
         deadline_misses=int(miss),

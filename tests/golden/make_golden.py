@@ -211,6 +211,11 @@ def main():
     sys.path.insert(0, REF)
     import slosim
 
+    if os.environ.get("GOLDEN_ONLY") == "policy":
+        make_event_golden(slosim)
+        make_policy_golden(slosim)
+        return
+
     out = {"meta": {"reference": "slosim @ /root/reference/pkg/src", "numpy": __import__("numpy").__version__}}
     # --- config 1: 6 rates x 2 pairs on gen_longtail(LongTailSpec())
     base = slosim.gen_longtail(slosim.LongTailSpec())
@@ -236,6 +241,127 @@ def main():
     path = os.path.join(HERE, "engine_golden.json.gz")
     with gzip.open(path, "wt", encoding="utf-8") as f:
         json.dump(out, f, sort_keys=True)
+    print("wrote", path, os.path.getsize(path))
+    make_event_golden(slosim)
+    make_policy_golden(slosim)
+
+
+def make_event_golden(slosim):
+    """Full reference event logs + token timestamps for the drop-in Simulation tests."""
+    from slosim.engine import Simulation
+
+    rng = random.Random(777)
+    out = []
+    for k in range(36):
+        wl, cfg = random_case(slosim, rng, k)
+        if rng.random() < 0.5:
+            wl = wl[: rng.randrange(1, len(wl) + 1)]
+        try:
+            sim = Simulation(cfg, wl, collect_events=True)
+            sim.run()
+        except slosim.ConfigurationError:
+            continue
+        out.append({
+            "workload": wl_to_json(wl), "config": cfg_to_json(cfg), "events": sim.events,
+            "requests": {r.id: {"tokens": r.token_timestamps, "tpf": r.t_prefill_finish} for r in sim.requests},
+            "lut_counts": sim.lut._counts, "lut_sums": sim.lut._sums,
+            "estimator": [sim.estimator.total_tokens, sim.estimator.total_busy_us],
+        })
+    path = os.path.join(HERE, "events_golden.json.gz")
+    with gzip.open(path, "wt", encoding="utf-8") as f:
+        json.dump(out, f, sort_keys=True)
+    print("wrote", path, len(out), os.path.getsize(path))
+
+
+def _rand_lut(slosim, rng):
+    bszs = sorted(rng.sample(range(1, 12), rng.randrange(1, 5)))
+    seqs = sorted(rng.sample(range(100, 200_000), rng.randrange(1, 7)))
+    lut = slosim.DecodeStepLUT(bsz_buckets=bszs, seq_buckets=seqs)
+    for b in bszs:
+        for sq in seqs:
+            if rng.random() < 0.8:
+                for _ in range(rng.randrange(1, 3)):
+                    lut.update(b, sq, rng.randrange(1_000, 80_000))
+    if lut.is_empty:
+        lut.update(bszs[0], seqs[0], 5_000)
+    return lut
+
+
+def make_policy_golden(slosim):
+    """Policy-level snapshot vectors: LUT lookups, decode/prefill selection, estimator, synth."""
+    rng = random.Random(4711)
+    lut_cases, dec_cases, pre_cases, synth_cases, est_cases = [], [], [], [], []
+    for _ in range(150):
+        lut = _rand_lut(slosim, rng)
+        qs = [(rng.randrange(1, 14), rng.choice([rng.randrange(1, 260_000)] + lut.seq_buckets)) for _ in range(40)]
+        lut_cases.append({"bsz": lut.bsz_buckets, "seq": lut.seq_buckets, "sums": lut._sums, "counts": lut._counts,
+                          "queries": qs, "values": [lut.lookup(b, sq) for b, sq in qs]})
+    slo = slosim.SLOConfig()
+    for k in range(400):
+        lut = _rand_lut(slosim, rng) if k % 2 else slosim.synth_profile_from_anchors(
+            [(1, 8192, 11_000), (1, 131072, 40_300)], 0.03)
+        active = []
+        for i in range(rng.randrange(1, 12 if k % 3 else 45)):
+            r = slosim.Request(id=f"d{rng.randrange(10**5)}_{i}", arrival_time=0,
+                               input_len=rng.randrange(1, 150_000), output_len=200)
+            r.record_first_token(0)
+            for j in range(rng.randrange(0, 40)):
+                r.record_decode_token(j + 1)
+            active.append(r)
+        t_now = rng.randrange(1, 2_000_000)
+        for pol in ("kairos-slack", "continuous"):
+            sel = slosim.DECODE_POLICIES[pol](active, t_now, slo, lut)
+            dec_cases.append({
+                "policy": pol, "bsz": lut.bsz_buckets, "seq": lut.seq_buckets, "sums": lut._sums,
+                "counts": lut._counts, "t_now": t_now,
+                "active": [[r.id, r.input_len, r.n_gen, r.t_first_token] for r in active],
+                "batch": sel.batch, "delayed": sel.delayed, "pred": sel.predicted_step_time_us,
+                "smin": None if math.isinf(sel.s_min_us) else sel.s_min_us, "fallback": sel.fallback,
+                "times": sel.admission_step_times_us})
+    for k in range(400):
+        est = slosim.PrefillThroughputEstimator.seeded(rng.randrange(5_000, 200_000), rng.randrange(300_000, 9_000_000))
+        q = []
+        for i in range(rng.randrange(0, 50 if k % 4 else 300)):
+            inp = rng.randrange(1, 60_000)
+            hit = rng.randrange(0, inp) if rng.random() < 0.3 else 0
+            done = rng.randrange(0, inp - hit + 1) if rng.random() < 0.3 else 0
+            q.append(slosim.Request(id=f"p{rng.randrange(10**5)}_{i}", arrival_time=rng.randrange(0, 4_000_000),
+                                    input_len=inp, output_len=1, prefix_hit_len=hit, prefill_done_tokens=done))
+        budget = rng.choice([1, 100, 4096, 8192, 20000])
+        t_now = rng.randrange(0, 3_000_000)
+        for pol in ("kairos-urgency", "fcfs", "sjf"):
+            b = slosim.PREFILL_POLICIES[pol](q, budget, t_now, est, slo)
+            pre_cases.append({
+                "policy": pol, "budget": budget, "t_now": t_now, "est": [est.total_tokens, est.total_busy_us],
+                "queue": [[r.id, r.arrival_time, r.input_len, r.prefix_hit_len, r.prefill_done_tokens] for r in q],
+                "entries": b.entries,
+                "finishes": slosim.prefill_sched.predict_finish_times(q, t_now, est) if pol == "fcfs" else None})
+    for _ in range(60):
+        anchors = [(1, rng.randrange(500, 150_000), rng.randrange(1_000, 60_000)) for _ in range(rng.randrange(1, 5))]
+        if rng.random() < 0.5:
+            anchors.append((rng.randrange(2, 300), rng.randrange(500, 300_000), rng.randrange(1_000, 90_000)))
+        gamma = rng.choice([0.0, 0.03, 0.05, 0.123])
+        w = rng.choice([0, 1, 7, 100])
+        bb = rng.choice([None, [1, 3, 8, 20]])
+        sb = rng.choice([None, [1000, 10000, 100000, 200000]])
+        import warnings
+        with warnings.catch_warnings():
+            warnings.simplefilter("ignore")
+            lut = slosim.synth_profile_from_anchors(anchors, gamma, bsz_buckets=bb, seq_buckets=sb, prior_weight=w)
+        qs = [(rng.randrange(1, 300), rng.randrange(1, 300_000)) for _ in range(20)]
+        synth_cases.append({"anchors": anchors, "gamma": gamma, "weight": w, "bsz": bb, "seq": sb,
+                            "sums": lut._sums, "counts": lut._counts,
+                            "formula": [slosim.decode_step_formula(sorted((s2, float(u)) for b2, s2, u in anchors if b2 == 1),
+                                                                   gamma, b2, s2) for b2, s2 in qs], "queries": qs})
+    for _ in range(100):
+        est = slosim.PrefillThroughputEstimator.seeded(rng.randrange(1, 10**9), rng.randrange(1, 10**11))
+        toks = [rng.randrange(0, 10**6) for _ in range(30)]
+        est_cases.append({"est": [est.total_tokens, est.total_busy_us], "tokens": toks,
+                          "out": [est.estimate_duration_us(x) for x in toks]})
+    path = os.path.join(HERE, "policy_golden.json.gz")
+    with gzip.open(path, "wt", encoding="utf-8") as f:
+        json.dump({"lut": lut_cases, "decode": dec_cases, "prefill": pre_cases, "synth": synth_cases,
+                   "estimate": est_cases}, f, sort_keys=True)
     print("wrote", path, os.path.getsize(path))
 
 
