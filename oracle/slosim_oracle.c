@@ -210,7 +210,12 @@ static int64_t decode_gt(const slosim_profile_t* P, const OLut* frozen, Pcg64* g
     return r < 1 ? 1 : r;
 }
 
-/* ------------------------------------------------------------- digest ---- */
+/* ------------------------------------------------------------- digest ----
+ * D <- fold((D ^ x) * phi64); decode members: sum of 32-bit (pos+1)*phi32. */
+static uint64_t dstep(uint64_t D, uint64_t x) {
+    uint64_t z = (D ^ x) * 0x9E3779B97F4A7C15ULL;
+    return z ^ (z >> 32);
+}
 static uint64_t mix64(uint64_t x) {
     x ^= x >> 30; x *= 0xbf58476d1ce4e5b9ULL;
     x ^= x >> 27; x *= 0x94d049bb133111ebULL;
@@ -390,10 +395,9 @@ static void run_instance(const slosim_batch_t* B, int64_t ii) {
             for (int e = 0; e < pf_k; e++) { S.done[pf_pos[e]] += (int32_t)pf_take[e]; tot += pf_take[e]; }
             S.est_tok += tot; S.est_busy += pf_dur;
             O->prefill_steps++;
-            uint64_t h = mix64((uint64_t)t ^ 0xA5A5A5A5A5A5A5A5ULL);
-            for (int e = 0; e < pf_k; e++) h = mix64(h ^ (((uint64_t)pf_pos[e] << 32) | (uint64_t)pf_take[e]));
-            h = mix64(h ^ (uint64_t)pf_dur);
-            D = mix64(D ^ h);
+            D = dstep(D, (uint64_t)t ^ 0xA5A5A5A5A5A5A5A5ULL);
+            for (int e = 0; e < pf_k; e++) D = dstep(D, ((uint64_t)pf_pos[e] << 32) | (uint64_t)pf_take[e]);
+            D = dstep(D, (uint64_t)pf_dur);
             if (T.buf) {
                 int64_t w[4] = {SLOSIM_EV_PREFILL_DONE, t, pf_dur, pf_k}; tr_put(&T, w, 4);
                 for (int e = 0; e < pf_k; e++) { int64_t x = ((int64_t)pf_pos[e] << 32) | pf_take[e]; tr_put(&T, &x, 1); }
@@ -415,10 +419,10 @@ static void run_instance(const slosim_batch_t* B, int64_t ii) {
         }
         /* decode completion engine.py:394-413 */
         if (dc_end == t) {
-            uint64_t s = 0;
+            uint32_t s = 0;
             for (int b = 0; b < dck; b++) {
                 int p = dcb[b];
-                s += mix64((uint64_t)p + 0x9E3779B97F4A7C15ULL);
+                s += ((uint32_t)p + 1u) * 0x9E3779B1u;
                 S.ngen[p] += 1;
                 if (t > S.tfirst[p] + (int64_t)S.ngen[p] * I->tpot_slo_us) S.miss[p]++;
                 S.tlast[p] = t;
@@ -430,9 +434,9 @@ static void run_instance(const slosim_batch_t* B, int64_t ii) {
             }
             if (use_lut) lut_update(&S.lut, dc_bsz, dc_max, dc_dur);
             O->decode_steps++;
-            uint64_t h = mix64((uint64_t)t ^ 0x5A5A5A5A5A5A5A5AULL);
-            h = mix64(h ^ s); h = mix64(h ^ (uint64_t)dck); h = mix64(h ^ (uint64_t)dc_dur);
-            D = mix64(D ^ h);
+            D = dstep(D, (uint64_t)t ^ 0x5A5A5A5A5A5A5A5AULL);
+            D = dstep(D, ((uint64_t)s << 32) | (uint32_t)dck);
+            D = dstep(D, (uint64_t)dc_dur);
             if (T.buf) {
                 int64_t w[5] = {SLOSIM_EV_DECODE_DONE, t, dc_dur, dc_bsz, dc_max}; tr_put(&T, w, 5);
                 for (int b = 0; b < dck; b++) { int64_t x = dcb[b]; tr_put(&T, &x, 1); }

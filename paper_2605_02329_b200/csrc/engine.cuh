@@ -156,26 +156,46 @@ __device__ int decode_scan(const LutMem* L, int an, const int32_t* ord, const in
     int64_t mseq = 0;
     int nd = 0;
     if (L->full && an <= 32 && !audit_delayed) {
+        // Dual-hypothesis rounds.  X: every candidate from s on is admitted, so
+        // lane r tests with |B| = b + (r - s) and t_cur = x[r-1]; the first lane
+        // whose test fails ends an admitted run (all X tests before it used the
+        // true state).  If that lane is s itself (nothing admitted this round),
+        // hypothesis Y (state unchanged) resolves the rest of the window: the
+        // first Y-admissible lane is admitted, or the window is rejected whole.
         bool have = lane < an;
         int i = have ? ord[lane] : 0;
         int64_t seq = have ? a_seq[i] : 1;
         ColSel cs = lut_col(L, seq);
         int s = 0;
         while (s < an) {
+            bool valid = have && lane >= s;
+            int64_t bx = b + (lane - s) + 1;
+            double x = valid ? lut_eval(L, lut_rows_nb(L, bx), cs) : 0.0;
+            double xprev = __shfl_up_sync(FULLMASK, x, 1);
+            double tprev = lane == s ? tcur : xprev;
+            int64_t bprev = bx - 1;
+            bool okx = valid && x <= smin && (bprev == 0 || xdiv((double)(bprev + 1), x) > xdiv((double)bprev, tprev));
+            unsigned failm = __ballot_sync(FULLMASK, valid && !okx);
+            int f = failm ? __ffs((int)failm) - 1 : an;
+            if (valid && lane < f) a_flag[i] |= 1;
+            if (f > s) {
+                b += f - s;
+                tcur = __shfl_sync(FULLMASK, x, f - 1);
+                mseq = __shfl_sync(FULLMASK, seq, f - 1);
+                s = f + 1;  // candidate f is rejected under the now-current state
+                continue;
+            }
+            // nothing admitted: candidate s rejected; test the rest with the unchanged state
             RowSel rs = lut_rows(L, b + 1);
             double thr = b ? xdiv((double)b, tcur) : 0.0;
-            bool valid = lane >= s && have;
-            double ts = 0.0;
-            bool cond = false;
-            if (valid) {
-                ts = lut_eval(L, rs, cs);
-                cond = ts <= smin && (b == 0 || xdiv((double)(b + 1), ts) > thr);
-            }
-            unsigned m = __ballot_sync(FULLMASK, cond);
+            bool vy = have && lane > s;
+            double y = vy ? lut_eval(L, rs, cs) : 0.0;
+            bool oky = vy && y <= smin && (b == 0 || xdiv((double)(b + 1), y) > thr);
+            unsigned m = __ballot_sync(FULLMASK, oky);
             if (!m) break;
             int j = __ffs((int)m) - 1;
             if (lane == j) a_flag[i] |= 1;
-            tcur = __shfl_sync(FULLMASK, ts, j);
+            tcur = __shfl_sync(FULLMASK, y, j);
             mseq = __shfl_sync(FULLMASK, seq, j);
             b++;
             s = j + 1;
@@ -468,6 +488,8 @@ __device__ void simulate(const Ctx& cx, int64_t ii, const WS& w, int lane) {
     int64_t kv = 0;
     int finished = 0;
     int32_t c_ttft = 0, c_tpot = 0, c_e2e = 0, ntps = 0, max_q = 0, max_a = 0;
+    int32_t l_tpot = 0, l_e2e = 0;  // per-lane partial counts, reduced once at the end
+    int64_t l_miss = 0;
     int64_t misses = 0, worst_wait = 0, psteps = 0, dsteps = 0, v_dec = 0, b_dec = 0, v_pre = 0, t_end = 0;
     uint64_t D = 0;
 
@@ -546,7 +568,7 @@ __device__ void simulate(const Ctx& cx, int64_t ii, const WS& w, int lane) {
             const int32_t* pf_qidx = w.i32(PF_QIDX);
             const int32_t* pf_take = w.i32(PF_TAKE);
             int64_t tot = 0;
-            uint64_t h = mix64((uint64_t)t ^ 0xA5A5A5A5A5A5A5A5ULL);
+            uint64_t h = dstep(D, (uint64_t)t ^ 0xA5A5A5A5A5A5A5A5ULL);
             if (T.buf && lane == 0) {
                 T.put(T.used, SLOSIM_EV_PREFILL_DONE); T.put(T.used + 1, t); T.put(T.used + 2, pf_dur); T.put(T.used + 3, pf_k);
             }
@@ -574,7 +596,7 @@ __device__ void simulate(const Ctx& cx, int64_t ii, const WS& w, int lane) {
                 tot += take;
                 // digest, batch order
                 int lim = pf_k - base < 32 ? pf_k - base : 32;
-                for (int j = 0; j < lim; j++) h = mix64(h ^ __shfl_sync(FULLMASK, word, j));
+                for (int j = 0; j < lim; j++) h = dstep(h, __shfl_sync(FULLMASK, word, j));
                 // completed requests leave the queue and start their KV transfer, batch order
                 int64_t delay = comp ? I->transfer_base_us + rint_i64(xmul((double)inp, I->transfer_per_token_us)) : 0;
                 unsigned cm = __ballot_sync(FULLMASK, comp);
@@ -605,8 +627,7 @@ __device__ void simulate(const Ctx& cx, int64_t ii, const WS& w, int lane) {
             est_tok += tot;
             est_busy += pf_dur;
             psteps++;
-            h = mix64(h ^ (uint64_t)pf_dur);
-            D = mix64(D ^ h);
+            D = dstep(h, (uint64_t)pf_dur);
             __syncwarp();
             if (ppol == SLOSIM_PREFILL_FCFS) {
                 qh += ncomp;  // FCFS completes a prefix of the queue
@@ -644,8 +665,8 @@ __device__ void simulate(const Ctx& cx, int64_t ii, const WS& w, int lane) {
             int32_t* a_flag = w.i32(A_FLAG);
             int64_t* a_tf = w.i64(A_TFIRST);
             double* tps_buf = w.f64(TPS);
-            uint64_t s = 0;
-            int64_t kv_rel = 0, mx = 0, miss_sum = 0;
+            uint32_t s = 0;
+            int64_t kv_rel = 0, mx = 0;
             int o = 0;
             int64_t tw0 = T.used + 5;
             int nmem = 0;
@@ -664,7 +685,7 @@ __device__ void simulate(const Ctx& cx, int64_t ii, const WS& w, int lane) {
                 if (inb) {
                     seq += 1;
                     int64_t ngen = seq - inp;
-                    s += mix64((uint64_t)pos + 0x9E3779B97F4A7C15ULL);
+                    s += member_hash((uint32_t)pos);
                     if (t > tf + ngen * tpot_slo) miss++;  // deadline_misses metrics.py:57-69
                     if (ngen == outl - 1) {
                         // request_metrics metrics.py:72-84 at retirement
@@ -688,11 +709,11 @@ __device__ void simulate(const Ctx& cx, int64_t ii, const WS& w, int lane) {
                 unsigned rmask = __ballot_sync(FULLMASK, retire);
                 if (retire) {
                     tps_buf[ntps + __popc(rmask & lanemask_lt(lane))] = tps;
-                    miss_sum += miss;
+                    l_miss += miss;
+                    l_tpot += tpm;
+                    l_e2e += tpm && (flag & 2);
                 }
                 ntps += __popc(rmask);
-                c_tpot += __popc(__ballot_sync(FULLMASK, retire && tpm));
-                c_e2e += __popc(__ballot_sync(FULLMASK, retire && tpm && (flag & 2)));
                 finished += __popc(rmask);
                 if (T.buf) {
                     unsigned bm = __ballot_sync(FULLMASK, inb);
@@ -713,20 +734,19 @@ __device__ void simulate(const Ctx& cx, int64_t ii, const WS& w, int lane) {
                 __syncwarp();
             }
             an = o;
-            amax = wmax64(mx);
-            misses += wsum64(miss_sum);
-            kv -= wsum64(kv_rel);
-            s = wsumu64(s);
+            amax = __reduce_max_sync(FULLMASK, (int)mx);
+            // retiring reservations: one REDUX when every lane's sum fits 26 bits
+            if (__all_sync(FULLMASK, kv_rel < (1LL << 26))) kv -= (int64_t)__reduce_add_sync(FULLMASK, (unsigned)kv_rel);
+            else kv -= wsum64(kv_rel);
+            s = __reduce_add_sync(FULLMASK, s);
             if (use_lut) {
                 if (lane == 0) lut_update(L, dc_bsz, dc_max, dc_dur);
                 __syncwarp();
             }
             dsteps++;
-            uint64_t h = mix64((uint64_t)t ^ 0x5A5A5A5A5A5A5A5AULL);
-            h = mix64(h ^ s);
-            h = mix64(h ^ (uint64_t)dc_bsz);
-            h = mix64(h ^ (uint64_t)dc_dur);
-            D = mix64(D ^ h);
+            D = dstep(D, (uint64_t)t ^ 0x5A5A5A5A5A5A5A5AULL);
+            D = dstep(D, ((uint64_t)s << 32) | (uint32_t)dc_bsz);
+            D = dstep(D, (uint64_t)dc_dur);
             if (T.buf && lane == 0) {
                 T.put(T.used, SLOSIM_EV_DECODE_DONE); T.put(T.used + 1, t); T.put(T.used + 2, dc_dur);
                 T.put(T.used + 3, dc_bsz); T.put(T.used + 4, dc_max);
@@ -786,7 +806,7 @@ __device__ void simulate(const Ctx& cx, int64_t ii, const WS& w, int lane) {
                 w.i32(A_FLAG)[d] = ttm ? 2 : 0;
             }
             an += __popc(dec);
-            amax = wmax64(adm && outl > 1 && inp > amax ? (int64_t)inp : amax);
+            amax = __reduce_max_sync(FULLMASK, (int)(adm && outl > 1 && inp > amax ? (int64_t)inp : amax));
             kv += wsum64(adm ? held : 0);
             ph += cnt;
             __syncwarp();
@@ -877,6 +897,9 @@ __device__ void simulate(const Ctx& cx, int64_t ii, const WS& w, int lane) {
     // ---- finalize: aggregate (metrics.py:109-144)
     double p50 = __longlong_as_double(0x7ff8000000000000LL), p90 = p50;
     __syncwarp();
+    c_tpot += __reduce_add_sync(FULLMASK, (unsigned)l_tpot);
+    c_e2e += __reduce_add_sync(FULLMASK, (unsigned)l_e2e);
+    misses += wsum64(l_miss);
     if (ntps > 0) {
         int64_t r50 = (int64_t)ceil(xmul(50 / 100.0, (double)ntps));
         int64_t r90 = (int64_t)ceil(xmul(90 / 100.0, (double)ntps));

@@ -168,6 +168,23 @@ __device__ __forceinline__ RowSel lut_rows(const LutMem* L, int64_t bsz) {
     return RowSel{i - 1, i, bsz - L->bb[i - 1], (int64_t)L->bb[i] - L->bb[i - 1]};
 }
 
+// Branch-free row selection for per-lane batch sizes (speculative scan).
+__device__ __forceinline__ RowSel lut_rows_nb(const LutMem* L, int64_t bsz) {
+    int i = lut_bidx(L, bsz);
+    int nb = L->nb;
+    int ic = i < nb ? i : nb - 1;
+    int64_t bi = L->bb[ic];
+    bool single = (i == 0) | (i == nb) | (bi == bsz);
+    int r1 = i == 0 ? 0 : (i == nb ? nb - 1 : (bi == bsz ? i : i - 1));
+    int64_t blo = L->bb[r1];
+    RowSel rs;
+    rs.r1 = r1;
+    rs.r2 = single ? -1 : i;
+    rs.num = single ? 0 : bsz - blo;
+    rs.den = single ? 1 : bi - blo;
+    return rs;
+}
+
 __device__ __forceinline__ double lut_eval(const LutMem* L, const RowSel& rs, const ColSel& cs) {
     int ns = L->ns;
     int k1 = rs.r1 * ns + cs.c;

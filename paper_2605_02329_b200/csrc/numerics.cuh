@@ -82,7 +82,15 @@ __device__ __forceinline__ int64_t ceil_muldiv(int64_t tokens, int64_t busy, int
     return (int64_t)(q + (r != 0));
 }
 
-// splitmix64 finalizer used by the decision digest.
+// Decision digest: D <- fold((D ^ x) * phi64),
+// and a 32-bit per-member hash summed over a decode batch (order-free).
+__device__ __forceinline__ uint64_t dstep(uint64_t D, uint64_t x) {
+    uint64_t z = (D ^ x) * 0x9E3779B97F4A7C15ULL;
+    return z ^ (z >> 32);
+}
+__device__ __forceinline__ uint32_t member_hash(uint32_t pos) { return (pos + 1u) * 0x9E3779B1u; }
+
+// splitmix64 finalizer.
 __device__ __forceinline__ uint64_t mix64(uint64_t x) {
     x ^= x >> 30; x *= 0xbf58476d1ce4e5b9ULL;
     x ^= x >> 27; x *= 0x94d049bb133111ebULL;

@@ -27,35 +27,31 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 M64 = (1 << 64) - 1
 
 
-def mix64(x):
-    x &= M64
-    x ^= x >> 30
-    x = (x * 0xBF58476D1CE4E5B9) & M64
-    x ^= x >> 27
-    x = (x * 0x94D049BB133111EB) & M64
-    x ^= x >> 31
-    return x
+def dstep(D, x):
+    z = ((D ^ x) * 0x9E3779B97F4A7C15) & M64
+    return z ^ (z >> 32)
 
 
 def digest_from_events(events, pos_of):
-    """Decision digest over the reference event log (PrefillStepDone/DecodeStepDone)."""
+    """Decision digest over the reference event log (PrefillStepDone/DecodeStepDone).
+
+    Per prefill step: t, each (pos, take) in batch order, duration; per decode
+    step: t, (sum of 32-bit member hashes << 32 | bsz), duration; each folded
+    with dstep (DESIGN.md "Decision digest")."""
     D = 0
     for ev in events:
         if ev["kind"] == "PrefillStepDone":
-            h = mix64(ev["t_us"] ^ 0xA5A5A5A5A5A5A5A5)
+            D = dstep(D, ev["t_us"] ^ 0xA5A5A5A5A5A5A5A5)
             for rid, take in ev["detail"]["batch"]:
-                h = mix64(h ^ ((pos_of[rid] << 32) | take))
-            h = mix64(h ^ ev["detail"]["duration_us"])
-            D = mix64(D ^ h)
+                D = dstep(D, (pos_of[rid] << 32) | take)
+            D = dstep(D, ev["detail"]["duration_us"])
         elif ev["kind"] == "DecodeStepDone":
             s = 0
             for rid in ev["detail"]["batch"]:
-                s = (s + mix64(pos_of[rid] + 0x9E3779B97F4A7C15)) & M64
-            h = mix64(ev["t_us"] ^ 0x5A5A5A5A5A5A5A5A)
-            h = mix64(h ^ s)
-            h = mix64(h ^ ev["detail"]["bsz"])
-            h = mix64(h ^ ev["detail"]["duration_us"])
-            D = mix64(D ^ h)
+                s = (s + (pos_of[rid] + 1) * 0x9E3779B1) & 0xFFFFFFFF
+            D = dstep(D, ev["t_us"] ^ 0x5A5A5A5A5A5A5A5A)
+            D = dstep(D, (s << 32) | ev["detail"]["bsz"])
+            D = dstep(D, ev["detail"]["duration_us"])
     return D
 
 
