@@ -260,10 +260,10 @@ def main():
     hist.zero_()
     for s in timed:
         off = s * slice_n
-        L.slosim_histogram(slice_n, ctypes.c_void_p(db.summaries.data_ptr() + off * 136),
+        L.slosim_histogram(slice_n, ctypes.c_void_p(db.summaries.data_ptr() + off * 144),
                            ctypes.c_void_p(cells.data_ptr() + off * 4), 1001, ctypes.c_void_p(hist.data_ptr()),
                            ctypes.c_void_p(stream.cuda_stream))
-    mine = torch.cat([db.summaries[s * slice_n * 136:(s + 1) * slice_n * 136] for s in timed])
+    mine = torch.cat([db.summaries[s * slice_n * 144:(s + 1) * slice_n * 144] for s in timed])
     gathered, hist = D.exchange(mine, hist)
     t_end.record()
     torch.cuda.synchronize()
@@ -377,7 +377,7 @@ def cpu_baseline(args, host_summ, slice_id, slice_n):
     ref = sw.packed.summaries
     got = host_summ[sel]
     mism = 0
-    for name in ref.dtype.names:
+    for name in [x for x in ref.dtype.names if x != "sim_cycles"]:
         a, b = got[name], ref[name]
         eq = np.array_equal(a, b, equal_nan=True) if a.dtype.kind == "f" else np.array_equal(a, b)
         mism += 0 if eq else 1

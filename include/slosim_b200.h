@@ -135,6 +135,7 @@ typedef struct slosim_summary {
     int64_t t_end_us;
     int64_t est_tokens, est_busy_us; /* final estimator state */
     int32_t max_queue, max_active;
+    int64_t sim_cycles;       /* SM clock cycles the instance occupied its warp (load-balance diagnostics) */
 } slosim_summary_t;
 
 /* Optional per-request rows (RequestMetrics metrics.py:14-23 + lifecycle times),
@@ -164,6 +165,7 @@ typedef struct slosim_batch {
     double* lut_out_sums;     /* optional final LUT per instance [n_instances][16*64] */
     int32_t* lut_out_counts;
     int64_t max_requests;     /* max n_requests over instances (sizes the per-warp workspace) */
+    const int64_t* order;     /* optional processing order (permutation of instance ids); NULL = identity */
 } slosim_batch_t;
 
 #define SLOSIM_F_ROWS 1          /* write per-request rows */

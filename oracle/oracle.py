@@ -26,7 +26,8 @@ def build():
 def lib():
     global _lib
     if _lib is None:
-        if not os.path.exists(LIB) or os.path.getmtime(LIB) < os.path.getmtime(os.path.join(HERE, "slosim_oracle.c")):
+        deps = [os.path.join(HERE, "slosim_oracle.c"), os.path.join(HERE, "..", "include", "slosim_b200.h")]
+        if not os.path.exists(LIB) or any(os.path.getmtime(LIB) < os.path.getmtime(d) for d in deps):
             build()
         L = ctypes.CDLL(LIB)
         vp = ctypes.c_void_p

@@ -117,6 +117,7 @@ class Summary(ctypes.Structure):
         ("est_busy_us", c_int64),
         ("max_queue", c_int32),
         ("max_active", c_int32),
+        ("sim_cycles", c_int64),
     ]
 
 
@@ -148,6 +149,7 @@ class Batch(ctypes.Structure):
         ("lut_out_sums", c_void_p),
         ("lut_out_counts", c_void_p),
         ("max_requests", c_int64),
+        ("order", c_void_p),
     ]
 
 
@@ -162,7 +164,7 @@ def summary_dtype():
             ("worst_queue_wait_us", "<i8"), ("prefill_steps", "<i8"), ("decode_steps", "<i8"),
             ("digest", "<u8"), ("v_dec", "<i8"), ("b_dec", "<i8"), ("v_pre", "<i8"),
             ("deadline_misses", "<i8"), ("t_end_us", "<i8"), ("est_tokens", "<i8"),
-            ("est_busy_us", "<i8"), ("max_queue", "<i4"), ("max_active", "<i4"),
+            ("est_busy_us", "<i8"), ("max_queue", "<i4"), ("max_active", "<i4"), ("sim_cycles", "<i8"),
         ]
     )
 
@@ -183,7 +185,7 @@ def instance_dtype():
     )
 
 
-assert ctypes.sizeof(Summary) == 136
+assert ctypes.sizeof(Summary) == 144
 assert ctypes.sizeof(Instance) == 128
 
 _HERE = os.path.dirname(os.path.abspath(__file__))

@@ -175,10 +175,26 @@ CONFIGS = {"config1": config1, "config2": config2, "config3": config3, "config4"
 
 
 # ------------------------------------------------------------ device run ---
+def schedule_order(instances: np.ndarray) -> np.ndarray:
+    """Processing order for the persistent kernel's work queue.
+
+    1. Group by decode policy (slack-guided first), so the warps resident on an
+       SM at any moment run the same specialised engine loop, whose instruction
+       working set then fits the SM's instruction cache.
+    2. Within a group, longest-first (LPT): the estimated cost is
+       n_requests x arrival stretch (the rescale factor; a low target rate means
+       many small decode steps), so the instances that finish last are short.
+    """
+    fac = instances["rescale_factor"].astype(np.float64)
+    cost = instances["n_requests"].astype(np.float64) * np.where(fac > 0, fac, 1.0)
+    dp = instances["decode_policy"].astype(np.int64)
+    return np.lexsort((-cost, -dp)).astype(np.int64)
+
+
 class DeviceBatch:
     """A packed batch resident in device memory (torch tensors as plumbing)."""
 
-    def __init__(self, packed: PackedBatch, device="cuda"):
+    def __init__(self, packed: PackedBatch, device="cuda", order: np.ndarray | None = None):
         import torch
 
         _abi.lib()
@@ -209,6 +225,9 @@ class DeviceBatch:
             for k, v in self.rows.items():
                 setattr(b.rows, k, v.data_ptr())
         b.max_requests = int(packed.instances["n_requests"].max()) if packed.n_instances else 0
+        self.order = t(schedule_order(packed.instances) if order is None else order)
+        b.order = self.order.data_ptr()
+        self._range_orders = {}
 
     def launch(self, stream=None) -> None:
         """Enqueue the engine on `stream` (default: torch's current stream)."""
@@ -224,6 +243,10 @@ class DeviceBatch:
         b.instances = self.instances.data_ptr() + start * ctypes.sizeof(_abi.Instance)
         b.summaries = self.summaries.data_ptr() + start * ctypes.sizeof(_abi.Summary)
         b.n_instances = count
+        if start not in self._range_orders or self._range_orders[start][0] != count:
+            o = schedule_order(self.packed.instances[start:start + count])
+            self._range_orders[start] = (count, self.torch.from_numpy(o).to(self.order.device))
+        b.order = self._range_orders[start][1].data_ptr()
         rc = _abi.lib().slosim_run_batch(ctypes.byref(b), ctypes.c_void_p(s.cuda_stream))
         if rc != _abi.OK:
             raise RuntimeError(f"slosim_run_batch failed ({rc}): {_abi.lib().slosim_last_error().decode()}")

@@ -276,7 +276,7 @@ __device__ __forceinline__ double selection_score(int64_t ttft_slo, int64_t fini
 
 // Packs the chunk budget from the queue [qh, qt) per policy (prefill_sched.py:93-145).
 // Writes (queue index, take) in batch order; returns the number of entries.
-__device__ int prefill_select(int policy, const WS& w, int qh, int qt, int64_t budget, int64_t t_now,
+__device__ __noinline__ int prefill_select(int policy, const WS& w, int qh, int qt, int64_t budget, int64_t t_now,
                               int64_t est_tok, int64_t est_busy, int64_t ttft_slo, int lane) {
     int32_t* pf_qidx = w.i32(PF_QIDX);
     int32_t* pf_take = w.i32(PF_TAKE);
@@ -369,7 +369,7 @@ __device__ __forceinline__ int64_t arrival_of(const int64_t* Tarr, double fac, i
 }
 
 // Pending list insert keeping (tpf, id_rank) order (engine.py:358).
-__device__ void pending_insert(const WS& w, int ph, int& pt, int64_t tpf, int32_t idr, int64_t ttr, int32_t pos,
+__device__ __noinline__ void pending_insert(const WS& w, int ph, int& pt, int64_t tpf, int32_t idr, int64_t ttr, int32_t pos,
                                int lane) {
     int64_t* pd_tpf = w.i64(PD_TPF);
     int64_t* pd_ttr = w.i64(PD_TTR);
@@ -403,7 +403,7 @@ __device__ void pending_insert(const WS& w, int ph, int& pt, int64_t tpf, int32_
 
 // Exact nearest-rank selection (metrics.py:87-92) of the r-th smallest of
 // n positive doubles by a bitwise radix descent on their IEEE bit patterns.
-__device__ double radix_select(const double* v, int n, int64_t r, int lane) {
+__device__ __noinline__ double radix_select(const double* v, int n, int64_t r, int lane) {
     uint64_t prefix = 0;
     int64_t need = r;
     for (int bit = 63; bit >= 0; bit--) {
@@ -428,7 +428,12 @@ __device__ void write_config_error(slosim_summary_t* out, int n) {
     *out = s;
 }
 
-__device__ void simulate(const Ctx& cx, int64_t ii, const WS& w, int lane) {
+// DP: decode policy (compile-time), FULL: event trace / per-request rows / LUT
+// export compiled in.  The throughput path runs simulate<DP, false>, whose hot
+// loop carries no tracing or row-output code.
+template <int DP, bool FULL>
+__device__ __noinline__ void simulate(const Ctx& cx, int64_t ii, const WS& w, int lane) {
+    const long long c0 = clock64();
     const slosim_batch_t* B = &cx.B;
     const slosim_instance_t* I = B->instances + ii;
     const int n = I->n_requests;
@@ -441,9 +446,9 @@ __device__ void simulate(const Ctx& cx, int64_t ii, const WS& w, int lane) {
     const int32_t* Thit = B->traces.prefix_hit_len + off;
     const int32_t* Tidr = B->traces.id_rank + off;
     const double fac = I->rescale_factor;
-    const bool rows = (B->flags & SLOSIM_F_ROWS) != 0;
+    const bool rows = FULL && (B->flags & SLOSIM_F_ROWS) != 0;
     const int64_t tpot_slo = I->tpot_slo_us, ttft_slo = I->ttft_slo_us, kv_cap = I->kv_capacity_tokens;
-    const int ppol = I->prefill_policy, dpol = I->decode_policy;
+    const int ppol = I->prefill_policy;
     const int64_t row0 = I->row_offset;
 
     // ---- Simulation.__init__ checks (engine.py:218-232)
@@ -458,14 +463,14 @@ __device__ void simulate(const Ctx& cx, int64_t ii, const WS& w, int lane) {
         if (lane == 0) write_config_error(B->summaries + ii, n);
         return;
     }
-    const bool use_lut = dpol == SLOSIM_DECODE_KAIROS_SLACK || (B->flags & (SLOSIM_F_ALWAYS_LUT | SLOSIM_F_EXPORT_LUT));
+    const bool use_lut = DP == SLOSIM_DECODE_KAIROS_SLACK || (B->flags & (SLOSIM_F_ALWAYS_LUT | SLOSIM_F_EXPORT_LUT));
     LutMem* L = w.lut();
     if (use_lut) lut_copy(L, ST, lane);
     int64_t est_tok = P->est_tokens, est_busy = P->est_busy_us;
     Pcg64 rng{I->rng_state_hi, I->rng_state_lo, I->rng_inc_hi, I->rng_inc_lo};
 
     TraceW T{nullptr, 0, 0};
-    if (B->trace_buf && I->trace_buf_offset >= 0) { T.buf = B->trace_buf + I->trace_buf_offset; T.cap = I->trace_buf_words; }
+    if (FULL && B->trace_buf && I->trace_buf_offset >= 0) { T.buf = B->trace_buf + I->trace_buf_offset; T.cap = I->trace_buf_words; }
 
     int32_t* q_pos = w.i32(Q_POS);
     int32_t* q_rem = w.i32(Q_REM);
@@ -513,7 +518,7 @@ __device__ void simulate(const Ctx& cx, int64_t ii, const WS& w, int lane) {
                     int32_t inp = Tinp[p];
                     int32_t full = inp - Thit[p];
                     q_pos[qi] = p; q_arr[qi] = a; q_inp[qi] = inp; q_full[qi] = full; q_rem[qi] = full;
-                    if (T.buf) {
+                    if (FULL && T.buf) {
                         int64_t o = T.used + 3 * lane;
                         T.put(o, SLOSIM_EV_ARRIVAL); T.put(o + 1, t); T.put(o + 2, p);
                     }
@@ -553,7 +558,7 @@ __device__ void simulate(const Ctx& cx, int64_t ii, const WS& w, int lane) {
                     int64_t jtpf = __shfl_sync(FULLMASK, tpf, j);
                     int32_t jpos = __shfl_sync(FULLMASK, pos, j);
                     pending_insert(w, ph, pt, jtpf, Tidr[jpos], t, jpos, lane);
-                    if (T.buf && lane == 0) { T.put(T.used, SLOSIM_EV_TRANSFER_DONE); T.put(T.used + 1, t); T.put(T.used + 2, jpos); }
+                    if (FULL && T.buf && lane == 0) { T.put(T.used, SLOSIM_EV_TRANSFER_DONE); T.put(T.used + 1, t); T.put(T.used + 2, jpos); }
                     T.used += 3;
                 }
             }
@@ -569,7 +574,7 @@ __device__ void simulate(const Ctx& cx, int64_t ii, const WS& w, int lane) {
             const int32_t* pf_take = w.i32(PF_TAKE);
             int64_t tot = 0;
             uint64_t h = dstep(D, (uint64_t)t ^ 0xA5A5A5A5A5A5A5A5ULL);
-            if (T.buf && lane == 0) {
+            if (FULL && T.buf && lane == 0) {
                 T.put(T.used, SLOSIM_EV_PREFILL_DONE); T.put(T.used + 1, t); T.put(T.used + 2, pf_dur); T.put(T.used + 3, pf_k);
             }
             T.used += 4;
@@ -601,13 +606,13 @@ __device__ void simulate(const Ctx& cx, int64_t ii, const WS& w, int lane) {
                 int64_t delay = comp ? I->transfer_base_us + rint_i64(xmul((double)inp, I->transfer_per_token_us)) : 0;
                 unsigned cm = __ballot_sync(FULLMASK, comp);
                 unsigned zm = __ballot_sync(FULLMASK, comp && delay == 0);
-                if (T.buf && comp && delay == 0) {
+                if (FULL && T.buf && comp && delay == 0) {
                     int64_t o = tw_transfers + 3 * (n0 + __popc(zm & lanemask_lt(lane)));
                     T.put(o, SLOSIM_EV_TRANSFER_DONE); T.put(o + 1, t); T.put(o + 2, pos);
                 }
                 n0 += __popc(zm);
                 ncomp += __popc(cm);
-                if (rows && comp) B->rows.t_prefill_finish[row0 + pos] = t;
+                if (FULL && rows && comp) B->rows.t_prefill_finish[row0 + pos] = t;
                 while (cm) {
                     int j = __ffs((int)cm) - 1;
                     cm &= cm - 1;
@@ -695,7 +700,7 @@ __device__ void simulate(const Ctx& cx, int64_t ii, const WS& w, int lane) {
                         tpm = tpot <= (double)tpot_slo;
                         tps = xdiv((double)(outl - 1), xdiv((double)span, 1e6));
                         kv_rel += (int64_t)inp + outl;
-                        if (rows) {
+                        if (FULL && rows) {
                             bool ttm = (flag & 2) != 0;
                             int64_t g = row0 + pos;
                             B->rows.mean_tpot_us[g] = tpot;
@@ -715,7 +720,7 @@ __device__ void simulate(const Ctx& cx, int64_t ii, const WS& w, int lane) {
                 }
                 ntps += __popc(rmask);
                 finished += __popc(rmask);
-                if (T.buf) {
+                if (FULL && T.buf) {
                     unsigned bm = __ballot_sync(FULLMASK, inb);
                     if (inb) T.put(tw0 + nmem + __popc(bm & lanemask_lt(lane)), pos);
                     nmem += __popc(bm);
@@ -747,11 +752,11 @@ __device__ void simulate(const Ctx& cx, int64_t ii, const WS& w, int lane) {
             D = dstep(D, (uint64_t)t ^ 0x5A5A5A5A5A5A5A5AULL);
             D = dstep(D, ((uint64_t)s << 32) | (uint32_t)dc_bsz);
             D = dstep(D, (uint64_t)dc_dur);
-            if (T.buf && lane == 0) {
+            if (FULL && T.buf && lane == 0) {
                 T.put(T.used, SLOSIM_EV_DECODE_DONE); T.put(T.used + 1, t); T.put(T.used + 2, dc_dur);
                 T.put(T.used + 3, dc_bsz); T.put(T.used + 4, dc_max);
             }
-            T.used += 5 + (T.buf ? nmem : 0);
+            T.used += 5 + (FULL && T.buf ? nmem : 0);
             dc_end = SLOSIM_INF64;
         }
 
@@ -775,11 +780,11 @@ __device__ void simulate(const Ctx& cx, int64_t ii, const WS& w, int lane) {
             if (adm) {
                 int64_t ttft = ttr - arrival_of(Tarr, fac, pos);
                 ttm = ttft <= ttft_slo;
-                if (T.buf) {
+                if (FULL && T.buf) {
                     int64_t o2 = T.used + 4 * lane;
                     T.put(o2, SLOSIM_EV_ADMIT); T.put(o2 + 1, t); T.put(o2 + 2, pos); T.put(o2 + 3, ttr);
                 }
-                if (rows) {
+                if (FULL && rows) {
                     int64_t g = row0 + pos;
                     B->rows.ttft_us[g] = ttft;
                     B->rows.t_first_token[g] = ttr;
@@ -838,7 +843,7 @@ __device__ void simulate(const Ctx& cx, int64_t ii, const WS& w, int lane) {
                         if (done == 0) {  // first time scheduled (engine.py:322)
                             int64_t wt = t - q_arr[qi];
                             ww = wt > ww ? wt : ww;
-                            if (rows) B->rows.first_sched_us[row0 + q_pos[qi]] = t;
+                            if (FULL && rows) B->rows.first_sched_us[row0 + q_pos[qi]] = t;
                         }
                     }
                     int lim = pf_k - base < 32 ? pf_k - base : 32;
@@ -859,7 +864,7 @@ __device__ void simulate(const Ctx& cx, int64_t ii, const WS& w, int lane) {
             int bsz = an;
             int64_t bmax = amax;
             dc_prefix = an;
-            if (dpol == SLOSIM_DECODE_KAIROS_SLACK) {
+            if (DP == SLOSIM_DECODE_KAIROS_SLACK) {
                 // select_decode_batch decode_sched.py:60-111
                 const int32_t* a_seq = w.i32(A_SEQ);
                 const int32_t* a_inp = w.i32(A_INP);
@@ -906,7 +911,7 @@ __device__ void simulate(const Ctx& cx, int64_t ii, const WS& w, int lane) {
         p50 = radix_select(w.f64(TPS), ntps, r50 < 1 ? 1 : r50, lane);
         p90 = radix_select(w.f64(TPS), ntps, r90 < 1 ? 1 : r90, lane);
     }
-    if ((B->flags & SLOSIM_F_EXPORT_LUT) && B->lut_out_sums) {
+    if (FULL && (B->flags & SLOSIM_F_EXPORT_LUT) && B->lut_out_sums) {
         const int FR = LUT_CELLS;
         const int nb = P->nb, ns = P->ns;
         for (int c = lane; c < FR; c += 32) {
@@ -916,10 +921,10 @@ __device__ void simulate(const Ctx& cx, int64_t ii, const WS& w, int lane) {
             B->lut_out_counts[ii * FR + c] = in ? L->cnt[i * ns + j] : 0;
         }
     }
-    if (T.buf && lane == 0 && T.used + 2 <= T.cap) { T.buf[T.used] = SLOSIM_EV_END; T.buf[T.used + 1] = T.used + 2; }
+    if (FULL && T.buf && lane == 0 && T.used + 2 <= T.cap) { T.buf[T.used] = SLOSIM_EV_END; T.buf[T.used + 1] = T.used + 2; }
     if (lane == 0) {
         slosim_summary_t s;
-        s.status = (finished == n ? SLOSIM_OK : -1) | ((T.buf && T.used + 2 > T.cap) ? 0x100 : 0);
+        s.status = (finished == n ? SLOSIM_OK : -1) | ((FULL && T.buf && T.used + 2 > T.cap) ? 0x100 : 0);
         s.n = n;
         s.ttft_met = c_ttft; s.tpot_met = c_tpot; s.e2e_met = c_e2e; s.n_tps = ntps;
         s.tps_p50 = p50; s.tps_p90 = p90;
@@ -931,12 +936,13 @@ __device__ void simulate(const Ctx& cx, int64_t ii, const WS& w, int lane) {
         s.t_end_us = t_end;
         s.est_tokens = est_tok; s.est_busy_us = est_busy;
         s.max_queue = max_q; s.max_active = max_a;
+        s.sim_cycles = clock64() - c0;
         B->summaries[ii] = s;
     }
 }
 
 #ifndef SLOSIM_MIN_BLOCKS
-#define SLOSIM_MIN_BLOCKS 3
+#define SLOSIM_MIN_BLOCKS 4
 #endif
 
 __global__ void __launch_bounds__(128, SLOSIM_MIN_BLOCKS)
@@ -945,12 +951,21 @@ __global__ void __launch_bounds__(128, SLOSIM_MIN_BLOCKS)
     const int64_t gw = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     WS w = make_ws(ws_base + (size_t)gw * ws_stride, cap);
     const int64_t N = cx.B.n_instances;
+    const bool full = (cx.B.flags & (SLOSIM_F_ROWS | SLOSIM_F_EXPORT_LUT)) || cx.B.trace_buf;
     for (;;) {
-        unsigned long long ii = 0;
-        if (lane == 0) ii = atomicAdd(work, 1ULL);
-        ii = __shfl_sync(FULLMASK, ii, 0);
-        if ((int64_t)ii >= N) break;
-        simulate(cx, (int64_t)ii, w, lane);
+        unsigned long long k = 0;
+        if (lane == 0) k = atomicAdd(work, 1ULL);
+        k = __shfl_sync(FULLMASK, k, 0);
+        if ((int64_t)k >= N) break;
+        const int64_t ii = cx.B.order ? cx.B.order[k] : (int64_t)k;
+        const bool kairos = cx.B.instances[ii].decode_policy == SLOSIM_DECODE_KAIROS_SLACK;
+        if (full) {
+            if (kairos) simulate<SLOSIM_DECODE_KAIROS_SLACK, true>(cx, ii, w, lane);
+            else simulate<SLOSIM_DECODE_CONTINUOUS, true>(cx, ii, w, lane);
+        } else {
+            if (kairos) simulate<SLOSIM_DECODE_KAIROS_SLACK, false>(cx, ii, w, lane);
+            else simulate<SLOSIM_DECODE_CONTINUOUS, false>(cx, ii, w, lane);
+        }
         __syncwarp();
     }
 }

@@ -76,7 +76,7 @@ __device__ __forceinline__ void lut_fix_slope(LutMem* L, int i, int j) {
 }
 
 // Single-thread (re)build of row i's means, mask and slopes.
-__device__ void lut_build_row(LutMem* L, int i) {
+__device__ __noinline__ void lut_build_row(LutMem* L, int i) {
     uint64_t m = 0;
     int c = i * L->ns;
     for (int j = 0; j < L->ns; j++) {

@@ -15,7 +15,7 @@ import numpy as np
 
 from . import _abi
 
-SUMMARY_BYTES = 136
+SUMMARY_BYTES = 144
 
 
 def slices_for_rank(n_slices: int, world: int, rank: int, steps: int, first_step: int = 0) -> list:

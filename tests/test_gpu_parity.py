@@ -81,7 +81,7 @@ def test_gpu_equals_oracle_on_config3_slice(lib):
     got = run_batch(sw.packed).copy()
     ref = config3(select=sel, synth=oracle.synth)
     oracle.run_batch(ref.packed, threads=8)
-    for k in ref.packed.summaries.dtype.names:
+    for k in [x for x in ref.packed.summaries.dtype.names if x != "sim_cycles"]:
         a, b = got[k], ref.packed.summaries[k]
         if a.dtype.kind == "f":
             assert np.array_equal(a, b, equal_nan=True), k
