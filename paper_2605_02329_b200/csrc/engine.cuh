@@ -110,7 +110,11 @@ struct TraceW {
 
 // ---------------------------------------------------- decode policy (K3) --
 // Orders the active set by (seq_len, id) (decode_sched.py:74) into ord[0..an).
-__device__ void decode_order(int an, const int32_t* a_seq, const int32_t* a_idr, int32_t* ord, int lane) {
+__device__ __noinline__ void decode_order_wide(int an, const int32_t* a_seq, const int32_t* a_idr, int32_t* ord,
+                                              int lane);
+
+__device__ __forceinline__ void decode_order(int an, const int32_t* a_seq, const int32_t* a_idr, int32_t* ord,
+                                             int lane) {
     if (an <= 32) {
         uint64_t key = lane < an ? (((uint64_t)(uint32_t)a_seq[lane] << 32) | (uint32_t)a_idr[lane]) : ~0ULL;
         int rank = 0;
@@ -119,7 +123,15 @@ __device__ void decode_order(int an, const int32_t* a_seq, const int32_t* a_idr,
             rank += kj < key;
         }
         if (lane < an) ord[rank] = lane;
+        __syncwarp();
     } else {
+        decode_order_wide(an, a_seq, a_idr, ord, lane);
+    }
+}
+
+__device__ __noinline__ void decode_order_wide(int an, const int32_t* a_seq, const int32_t* a_idr, int32_t* ord,
+                                              int lane) {
+    {
         for (int i0 = 0; i0 < an; i0 += 32) {
             int i = i0 + lane;
             uint64_t key = i < an ? (((uint64_t)(uint32_t)a_seq[i] << 32) | (uint32_t)a_idr[i]) : ~0ULL;
@@ -148,9 +160,15 @@ __device__ void decode_order(int an, const int32_t* a_seq, const int32_t* a_idr,
 // selects the rows for |B|+1.  Sets a_flag bit0 of admitted entries; returns
 // |B| (0 = fallback).  Optional audit outputs (snapshot API): admitted order,
 // delayed order, admission times.
-__device__ int decode_scan(const LutMem* L, int an, const int32_t* ord, const int32_t* a_seq, int32_t* a_flag,
-                           double smin, double* tcur_out, int64_t* maxseq_out, int32_t* audit_batch,
-                           int32_t* audit_delayed, double* audit_times, int* n_delayed, int lane) {
+__device__ __noinline__ int decode_scan_general(const LutMem* L, int an, const int32_t* ord, const int32_t* a_seq,
+                                                int32_t* a_flag, double smin, double* tcur_out, int64_t* maxseq_out,
+                                                int32_t* audit_batch, int32_t* audit_delayed, double* audit_times,
+                                                int* n_delayed, int lane);
+
+__device__ __forceinline__ int decode_scan(const LutMem* L, int an, const int32_t* ord, const int32_t* a_seq,
+                                           int32_t* a_flag, double smin, double* tcur_out, int64_t* maxseq_out,
+                                           int32_t* audit_batch, int32_t* audit_delayed, double* audit_times,
+                                           int* n_delayed, int lane) {
     int b = 0;
     double tcur = 0.0;
     int64_t mseq = 0;
@@ -205,6 +223,18 @@ __device__ int decode_scan(const LutMem* L, int an, const int32_t* ord, const in
         *maxseq_out = mseq;
         return b;
     }
+    return decode_scan_general(L, an, ord, a_seq, a_flag, smin, tcur_out, maxseq_out, audit_batch, audit_delayed,
+                               audit_times, n_delayed, lane);
+}
+
+__device__ __noinline__ int decode_scan_general(const LutMem* L, int an, const int32_t* ord, const int32_t* a_seq,
+                                                int32_t* a_flag, double smin, double* tcur_out, int64_t* maxseq_out,
+                                                int32_t* audit_batch, int32_t* audit_delayed, double* audit_times,
+                                                int* n_delayed, int lane) {
+    int b = 0;
+    double tcur = 0.0;
+    int64_t mseq = 0;
+    int nd = 0;
     int s = 0;
     while (s < an) {
         int r = s + lane;
@@ -428,239 +458,437 @@ __device__ void write_config_error(slosim_summary_t* out, int n) {
     *out = s;
 }
 
+// ------------------------------------------------------ instance state --
+// All per-instance state of one simulation.  It lives in registers inside the
+// hot decode loop of simulate(); the rare per-request events (arrival,
+// transfer, prefill completion/start, admission) are out-of-line functions
+// that take it by reference, so their code stays out of the hot loop's
+// instruction working set (the SM instruction cache is ~32 KB).
+struct Sim {
+    const slosim_batch_t* B;
+    const slosim_instance_t* I;
+    const slosim_profile_t* P;
+    const int64_t* Tarr;
+    const int32_t *Tinp, *Tout, *Thit, *Tidr;
+    LutMem* L;
+    WS w;
+    double fac;
+    int64_t ii, row0, tpot_slo, ttft_slo, kv_cap;
+    int n, ppol;
+    bool rows;
+    // event state
+    int ai, qh, qt, pf_k, trn, ph, pt, an, dc_prefix, finished;
+    int64_t next_arr, pf_end, pf_dur, tr_min, dc_end, dc_dur, dc_bsz, dc_max, amax, kv, est_tok, est_busy;
+    // counters
+    int32_t c_ttft, c_tpot, c_e2e, ntps, max_q, max_a;
+    int64_t misses, worst_wait, psteps, dsteps, v_dec, b_dec, v_pre, t_end;
+    uint64_t D;
+    TraceW T;
+};
+
+// ---- arrivals (engine.py:288-291): a contiguous run of the trace
+template <bool FULL>
+__device__ __noinline__ void on_arrivals(Sim& S, int64_t t, int lane) {
+    int32_t* q_pos = S.w.i32(Q_POS);
+    int32_t* q_rem = S.w.i32(Q_REM);
+    int32_t* q_full = S.w.i32(Q_FULL);
+    int32_t* q_inp = S.w.i32(Q_INP);
+    int64_t* q_arr = S.w.i64(Q_ARR);
+    for (;;) {
+        int p = S.ai + lane;
+        int64_t a = p < S.n ? arrival_of(S.Tarr, S.fac, p) : SLOSIM_INF64;
+        unsigned m = __ballot_sync(FULLMASK, a == t);
+        int cnt = __popc(m);
+        if (lane < cnt) {
+            int qi = S.qt + lane;
+            int32_t inp = S.Tinp[p];
+            int32_t full = inp - S.Thit[p];
+            q_pos[qi] = p; q_arr[qi] = a; q_inp[qi] = inp; q_full[qi] = full; q_rem[qi] = full;
+            if (FULL && S.T.buf) {
+                int64_t o = S.T.used + 3 * lane;
+                S.T.put(o, SLOSIM_EV_ARRIVAL); S.T.put(o + 1, t); S.T.put(o + 2, p);
+            }
+        }
+        S.T.used += 3 * cnt;
+        S.qt += cnt;
+        S.ai += cnt;
+        if (cnt < 32) { S.next_arr = __shfl_sync(FULLMASK, a, cnt); break; }
+    }
+    __syncwarp();
+}
+
+// ---- transfers due now that were pushed at earlier instants (engine.py:294-298)
+template <bool FULL>
+__device__ __noinline__ void on_transfers(Sim& S, int64_t t, int lane) {
+    int64_t* tr_t = S.w.i64(TR_T);
+    int64_t* tr_tpf = S.w.i64(TR_TPF);
+    int32_t* tr_pos = S.w.i32(TR_POS);
+    int m_keep = 0;
+    for (int base = 0; base < S.trn; base += 32) {
+        int k = base + lane;
+        bool v = k < S.trn;
+        int64_t tt = v ? tr_t[k] : 0, tpf = v ? tr_tpf[k] : 0;
+        int32_t pos = v ? tr_pos[k] : 0;
+        bool due = v && tt == t;
+        unsigned dm = __ballot_sync(FULLMASK, due);
+        unsigned km = __ballot_sync(FULLMASK, v && !due);
+        __syncwarp();
+        if (v && !due) {
+            int o = m_keep + __popc(km & lanemask_lt(lane));
+            tr_t[o] = tt; tr_tpf[o] = tpf; tr_pos[o] = pos;
+        }
+        m_keep += __popc(km);
+        __syncwarp();
+        while (dm) {
+            int j = __ffs((int)dm) - 1;
+            dm &= dm - 1;
+            int64_t jtpf = __shfl_sync(FULLMASK, tpf, j);
+            int32_t jpos = __shfl_sync(FULLMASK, pos, j);
+            pending_insert(S.w, S.ph, S.pt, jtpf, S.Tidr[jpos], t, jpos, lane);
+            if (FULL && S.T.buf && lane == 0) {
+                S.T.put(S.T.used, SLOSIM_EV_TRANSFER_DONE); S.T.put(S.T.used + 1, t); S.T.put(S.T.used + 2, jpos);
+            }
+            S.T.used += 3;
+        }
+    }
+    S.trn = m_keep;
+    int64_t mn = SLOSIM_INF64;
+    for (int k = lane; k < S.trn; k += 32) { int64_t tt = tr_t[k]; mn = tt < mn ? tt : mn; }
+    S.tr_min = wmin64(mn);
+}
+
+// ---- prefill step completion (engine.py:327-350)
+template <bool FULL>
+__device__ __noinline__ void on_prefill_done(Sim& S, int64_t t, int lane) {
+    const slosim_instance_t* I = S.I;
+    int32_t* q_pos = S.w.i32(Q_POS);
+    int32_t* q_rem = S.w.i32(Q_REM);
+    int32_t* q_full = S.w.i32(Q_FULL);
+    int32_t* q_inp = S.w.i32(Q_INP);
+    int64_t* q_arr = S.w.i64(Q_ARR);
+    const int32_t* pf_qidx = S.w.i32(PF_QIDX);
+    const int32_t* pf_take = S.w.i32(PF_TAKE);
+    const int pf_k = S.pf_k;
+    int64_t tot = 0;
+    uint64_t h = dstep(S.D, (uint64_t)t ^ 0xA5A5A5A5A5A5A5A5ULL);
+    if (FULL && S.T.buf && lane == 0) {
+        S.T.put(S.T.used, SLOSIM_EV_PREFILL_DONE); S.T.put(S.T.used + 1, t); S.T.put(S.T.used + 2, S.pf_dur);
+        S.T.put(S.T.used + 3, pf_k);
+    }
+    S.T.used += 4;
+    int64_t tw_transfers = S.T.used + pf_k;  // delay-0 TransferDone records follow the batch list
+    int ncomp = 0, n0 = 0;
+    for (int base = 0; base < pf_k; base += 32) {
+        int e = base + lane;
+        bool v = e < pf_k;
+        int64_t take = 0;
+        int32_t pos = 0, inp = 0;
+        bool comp = false;
+        uint64_t word = 0;
+        if (v) {
+            int qi = pf_qidx[e];
+            take = pf_take[e];
+            int32_t rem = q_rem[qi] - (int32_t)take;
+            q_rem[qi] = rem;
+            pos = q_pos[qi];
+            inp = q_inp[qi];
+            comp = rem == 0;
+            word = ((uint64_t)(uint32_t)pos << 32) | (uint32_t)take;
+            if (FULL) S.T.put(S.T.used + e, (int64_t)word);
+        }
+        tot += take;
+        int lim = pf_k - base < 32 ? pf_k - base : 32;
+        for (int j = 0; j < lim; j++) h = dstep(h, __shfl_sync(FULLMASK, word, j));
+        // completed requests leave the queue and start their KV transfer, batch order
+        int64_t delay = comp ? I->transfer_base_us + rint_i64(xmul((double)inp, I->transfer_per_token_us)) : 0;
+        unsigned cm = __ballot_sync(FULLMASK, comp);
+        unsigned zm = __ballot_sync(FULLMASK, comp && delay == 0);
+        if (FULL && S.T.buf && comp && delay == 0) {
+            int64_t o = tw_transfers + 3 * (n0 + __popc(zm & lanemask_lt(lane)));
+            S.T.put(o, SLOSIM_EV_TRANSFER_DONE); S.T.put(o + 1, t); S.T.put(o + 2, pos);
+        }
+        n0 += __popc(zm);
+        ncomp += __popc(cm);
+        if (FULL && S.rows && comp) S.B->rows.t_prefill_finish[S.row0 + pos] = t;
+        while (cm) {
+            int j = __ffs((int)cm) - 1;
+            cm &= cm - 1;
+            int32_t jpos = __shfl_sync(FULLMASK, pos, j);
+            int64_t jdel = __shfl_sync(FULLMASK, delay, j);
+            if (jdel == 0) {
+                pending_insert(S.w, S.ph, S.pt, t, S.Tidr[jpos], t, jpos, lane);
+            } else {
+                if (lane == 0) { S.w.i64(TR_T)[S.trn] = t + jdel; S.w.i64(TR_TPF)[S.trn] = t; S.w.i32(TR_POS)[S.trn] = jpos; }
+                S.trn++;
+                S.tr_min = t + jdel < S.tr_min ? t + jdel : S.tr_min;
+            }
+        }
+    }
+    S.T.used += pf_k + 3 * n0;
+    tot = wsum64(tot);
+    S.est_tok += tot;
+    S.est_busy += S.pf_dur;
+    S.psteps++;
+    S.D = dstep(h, (uint64_t)S.pf_dur);
+    __syncwarp();
+    if (S.ppol == SLOSIM_PREFILL_FCFS) {
+        S.qh += ncomp;  // FCFS completes a prefix of the queue
+    } else if (ncomp) {
+        int o = S.qh;
+        for (int base = S.qh; base < S.qt; base += 32) {
+            int qi = base + lane;
+            bool v = qi < S.qt;
+            int32_t pos = 0, rem = 0, full = 0, inp = 0;
+            int64_t a = 0;
+            if (v) { pos = q_pos[qi]; rem = q_rem[qi]; full = q_full[qi]; inp = q_inp[qi]; a = q_arr[qi]; }
+            bool keep = v && rem > 0;
+            unsigned km = __ballot_sync(FULLMASK, keep);
+            __syncwarp();
+            if (keep) {
+                int d = o + __popc(km & lanemask_lt(lane));
+                q_pos[d] = pos; q_rem[d] = rem; q_full[d] = full; q_inp[d] = inp; q_arr[d] = a;
+            }
+            o += __popc(km);
+            __syncwarp();
+        }
+        S.qt = o;
+    }
+    S.pf_end = SLOSIM_INF64;
+}
+
+// ---- admission under the KV reservation (engine.py:355-375)
+template <bool FULL>
+__device__ __noinline__ void on_admit(Sim& S, int64_t t, int lane) {
+    const slosim_batch_t* B = S.B;
+    while (S.pt > S.ph) {
+        int k = S.ph + lane;
+        bool v = k < S.pt;
+        int32_t pos = v ? S.w.i32(PD_POS)[k] : 0;
+        int32_t outl = v ? S.Tout[pos] : 0, inp = v ? S.Tinp[pos] : 0;
+        int64_t need = (int64_t)inp + outl;
+        int64_t held = (v && outl > 1) ? need : 0;
+        int64_t excl = wscan_incl64(held, lane) - held;
+        bool ok = v && S.kv + excl + need <= S.kv_cap;
+        unsigned vm = __ballot_sync(FULLMASK, v);
+        unsigned okm = __ballot_sync(FULLMASK, ok);
+        unsigned fail = vm & ~okm;
+        int cnt = fail ? __ffs((int)fail) - 1 : __popc(vm);
+        bool adm = lane < cnt;
+        int64_t ttr = adm ? S.w.i64(PD_TTR)[k] : 0;
+        bool ttm = false;
+        if (adm) {
+            int64_t ttft = ttr - arrival_of(S.Tarr, S.fac, pos);
+            ttm = ttft <= S.ttft_slo;
+            if (FULL && S.T.buf) {
+                int64_t o2 = S.T.used + 4 * lane;
+                S.T.put(o2, SLOSIM_EV_ADMIT); S.T.put(o2 + 1, t); S.T.put(o2 + 2, pos); S.T.put(o2 + 3, ttr);
+            }
+            if (FULL && S.rows) {
+                int64_t g = S.row0 + pos;
+                B->rows.ttft_us[g] = ttft;
+                B->rows.t_first_token[g] = ttr;
+                if (outl == 1) {
+                    B->rows.mean_tpot_us[g] = 0.0;
+                    B->rows.decode_tps[g] = __longlong_as_double(0x7ff8000000000000LL);
+                    B->rows.met_flags[g] = (uint8_t)((ttm ? 1 : 0) | 2 | (ttm ? 4 : 0));
+                    B->rows.deadline_misses[g] = 0;
+                    B->rows.t_last_token[g] = ttr;
+                }
+            }
+        }
+        S.T.used += 4 * cnt;
+        S.c_ttft += __popc(__ballot_sync(FULLMASK, adm && ttm));
+        unsigned one = __ballot_sync(FULLMASK, adm && outl == 1);
+        S.c_tpot += __popc(one);
+        S.c_e2e += __popc(__ballot_sync(FULLMASK, adm && outl == 1 && ttm));
+        S.finished += __popc(one);
+        unsigned dec = __ballot_sync(FULLMASK, adm && outl > 1);
+        if (adm && outl > 1) {
+            int d = S.an + __popc(dec & lanemask_lt(lane));
+            S.w.i32(A_POS)[d] = pos; S.w.i32(A_SEQ)[d] = inp; S.w.i32(A_IDR)[d] = S.w.i32(PD_IDR)[k];
+            S.w.i32(A_OUT)[d] = outl; S.w.i32(A_INP)[d] = inp; S.w.i32(A_MISS)[d] = 0; S.w.i64(A_TFIRST)[d] = ttr;
+            S.w.i32(A_FLAG)[d] = ttm ? 2 : 0;
+        }
+        S.an += __popc(dec);
+        S.amax = __reduce_max_sync(FULLMASK, (int)(adm && outl > 1 && inp > S.amax ? (int64_t)inp : S.amax));
+        S.kv += wsum64(adm ? held : 0);
+        S.ph += cnt;
+        __syncwarp();
+        if (cnt < 32) break;
+    }
+}
+
+// ---- start a prefill step (engine.py:307-325)
+template <bool FULL>
+__device__ __noinline__ void on_prefill_start(Sim& S, int64_t t, int lane) {
+    const slosim_profile_t* P = S.P;
+    int qlen = S.qt - S.qh;
+    S.v_pre += qlen;
+    S.max_q = qlen > S.max_q ? qlen : S.max_q;
+    S.pf_k = prefill_select(S.ppol, S.w, S.qh, S.qt, S.I->chunk_budget, t, S.est_tok, S.est_busy, S.ttft_slo, lane);
+    if (S.pf_k <= 0) return;
+    // ground-truth duration: ordered sum of curve increments (engine.py:175-183)
+    const int32_t* pf_qidx = S.w.i32(PF_QIDX);
+    const int32_t* pf_take = S.w.i32(PF_TAKE);
+    const int32_t* q_full = S.w.i32(Q_FULL);
+    const int32_t* q_rem = S.w.i32(Q_REM);
+    const int64_t* q_arr = S.w.i64(Q_ARR);
+    const int n_curve = P->n_curve;
+    double total = 0.0;
+    int64_t ww = 0;
+    for (int base = 0; base < S.pf_k; base += 32) {
+        int e = base + lane;
+        double term = 0.0;
+        if (e < S.pf_k) {
+            int qi = pf_qidx[e];
+            int64_t take = pf_take[e];
+            int64_t done = (int64_t)q_full[qi] - q_rem[qi];
+            term = xsub(curve_at(n_curve, P->curve_x, P->curve_y, done + take),
+                        curve_at(n_curve, P->curve_x, P->curve_y, done));
+            if (done == 0) {  // first time scheduled (engine.py:322)
+                int64_t wt = t - q_arr[qi];
+                ww = wt > ww ? wt : ww;
+                if (FULL && S.rows) S.B->rows.first_sched_us[S.row0 + S.w.i32(Q_POS)[qi]] = t;
+            }
+        }
+        int lim = S.pf_k - base < 32 ? S.pf_k - base : 32;
+        for (int j = 0; j < lim; j++) total = xadd(total, __shfl_sync(FULLMASK, term, j));
+    }
+    ww = wmax64(ww);
+    S.worst_wait = ww > S.worst_wait ? ww : S.worst_wait;
+    int64_t d = rint_i64(total);
+    S.pf_dur = d < 1 ? 1 : d;
+    S.pf_end = t + S.pf_dur;
+}
+
+// ---- finalize: aggregate (metrics.py:109-144)
+template <bool FULL>
+__device__ __noinline__ void on_finalize(Sim& S, int32_t l_tpot, int32_t l_e2e, int64_t l_miss, long long c0, int lane) {
+    const slosim_batch_t* B = S.B;
+    double p50 = __longlong_as_double(0x7ff8000000000000LL), p90 = p50;
+    __syncwarp();
+    S.c_tpot += __reduce_add_sync(FULLMASK, (unsigned)l_tpot);
+    S.c_e2e += __reduce_add_sync(FULLMASK, (unsigned)l_e2e);
+    S.misses += wsum64(l_miss);
+    if (S.ntps > 0) {
+        int64_t r50 = (int64_t)ceil(xmul(50 / 100.0, (double)S.ntps));
+        int64_t r90 = (int64_t)ceil(xmul(90 / 100.0, (double)S.ntps));
+        p50 = radix_select(S.w.f64(TPS), S.ntps, r50 < 1 ? 1 : r50, lane);
+        p90 = radix_select(S.w.f64(TPS), S.ntps, r90 < 1 ? 1 : r90, lane);
+    }
+    if (FULL && (B->flags & SLOSIM_F_EXPORT_LUT) && B->lut_out_sums) {
+        const int FR = LUT_CELLS;
+        const int nb = S.P->nb, ns = S.P->ns;
+        for (int c = lane; c < FR; c += 32) {
+            int i = c / SLOSIM_MAX_SEQ_BUCKETS, j = c % SLOSIM_MAX_SEQ_BUCKETS;
+            bool in = i < nb && j < ns;
+            B->lut_out_sums[S.ii * FR + c] = in ? S.L->sum[i * ns + j] : 0.0;
+            B->lut_out_counts[S.ii * FR + c] = in ? S.L->cnt[i * ns + j] : 0;
+        }
+    }
+    const TraceW& T = S.T;
+    if (FULL && T.buf && lane == 0 && T.used + 2 <= T.cap) { T.buf[T.used] = SLOSIM_EV_END; T.buf[T.used + 1] = T.used + 2; }
+    if (lane == 0) {
+        slosim_summary_t s;
+        s.status = (S.finished == S.n ? SLOSIM_OK : -1) | ((FULL && T.buf && T.used + 2 > T.cap) ? 0x100 : 0);
+        s.n = S.n;
+        s.ttft_met = S.c_ttft; s.tpot_met = S.c_tpot; s.e2e_met = S.c_e2e; s.n_tps = S.ntps;
+        s.tps_p50 = p50; s.tps_p90 = p90;
+        s.worst_queue_wait_us = S.worst_wait;
+        s.prefill_steps = S.psteps; s.decode_steps = S.dsteps;
+        s.digest = S.D;
+        s.v_dec = S.v_dec; s.b_dec = S.b_dec; s.v_pre = S.v_pre;
+        s.deadline_misses = S.misses;
+        s.t_end_us = S.t_end;
+        s.est_tokens = S.est_tok; s.est_busy_us = S.est_busy;
+        s.max_queue = S.max_q; s.max_active = S.max_a;
+        s.sim_cycles = clock64() - c0;
+        B->summaries[S.ii] = s;
+    }
+}
+
 // DP: decode policy (compile-time), FULL: event trace / per-request rows / LUT
 // export compiled in.  The throughput path runs simulate<DP, false>, whose hot
 // loop carries no tracing or row-output code.
 template <int DP, bool FULL>
 __device__ __noinline__ void simulate(const Ctx& cx, int64_t ii, const WS& w, int lane) {
     const long long c0 = clock64();
-    const slosim_batch_t* B = &cx.B;
-    const slosim_instance_t* I = B->instances + ii;
-    const int n = I->n_requests;
+    Sim S;
+    S.B = &cx.B;
+    S.ii = ii;
+    S.I = S.B->instances + ii;
+    const slosim_instance_t* I = S.I;
+    S.n = I->n_requests;
     const int pid = I->profile_id;
-    const slosim_profile_t* P = B->profiles + pid;
+    S.P = S.B->profiles + pid;
     const int64_t off = I->trace_offset;
-    const int64_t* Tarr = B->traces.arrival_us + off;
-    const int32_t* Tinp = B->traces.input_len + off;
-    const int32_t* Tout = B->traces.output_len + off;
-    const int32_t* Thit = B->traces.prefix_hit_len + off;
-    const int32_t* Tidr = B->traces.id_rank + off;
-    const double fac = I->rescale_factor;
-    const bool rows = FULL && (B->flags & SLOSIM_F_ROWS) != 0;
-    const int64_t tpot_slo = I->tpot_slo_us, ttft_slo = I->ttft_slo_us, kv_cap = I->kv_capacity_tokens;
-    const int ppol = I->prefill_policy;
-    const int64_t row0 = I->row_offset;
+    S.Tarr = S.B->traces.arrival_us + off;
+    S.Tinp = S.B->traces.input_len + off;
+    S.Tout = S.B->traces.output_len + off;
+    S.Thit = S.B->traces.prefix_hit_len + off;
+    S.Tidr = S.B->traces.id_rank + off;
+    S.fac = I->rescale_factor;
+    S.rows = FULL && (S.B->flags & SLOSIM_F_ROWS) != 0;
+    S.tpot_slo = I->tpot_slo_us;
+    S.ttft_slo = I->ttft_slo_us;
+    S.kv_cap = I->kv_capacity_tokens;
+    S.ppol = I->prefill_policy;
+    S.row0 = I->row_offset;
+    S.w = w;
 
     // ---- Simulation.__init__ checks (engine.py:218-232)
     int64_t worst = 0;
-    for (int p = lane; p < n; p += 32) {
-        int64_t need = (int64_t)Tinp[p] + Tout[p];
+#pragma unroll 1
+    for (int p = lane; p < S.n; p += 32) {
+        int64_t need = (int64_t)S.Tinp[p] + S.Tout[p];
         worst = need > worst ? need : worst;
     }
     worst = wmax64(worst);
     const LutMem* ST = cx.sched_tab + pid;
-    if (worst > kv_cap || ST->rowmask == 0) {
-        if (lane == 0) write_config_error(B->summaries + ii, n);
+    if (worst > S.kv_cap || ST->rowmask == 0) {
+        if (lane == 0) write_config_error(S.B->summaries + ii, S.n);
         return;
     }
-    const bool use_lut = DP == SLOSIM_DECODE_KAIROS_SLACK || (B->flags & (SLOSIM_F_ALWAYS_LUT | SLOSIM_F_EXPORT_LUT));
-    LutMem* L = w.lut();
+    const bool use_lut = DP == SLOSIM_DECODE_KAIROS_SLACK || (S.B->flags & (SLOSIM_F_ALWAYS_LUT | SLOSIM_F_EXPORT_LUT));
+    S.L = w.lut();
+    LutMem* L = S.L;
     if (use_lut) lut_copy(L, ST, lane);
-    int64_t est_tok = P->est_tokens, est_busy = P->est_busy_us;
+    S.est_tok = S.P->est_tokens;
+    S.est_busy = S.P->est_busy_us;
     Pcg64 rng{I->rng_state_hi, I->rng_state_lo, I->rng_inc_hi, I->rng_inc_lo};
-
-    TraceW T{nullptr, 0, 0};
-    if (FULL && B->trace_buf && I->trace_buf_offset >= 0) { T.buf = B->trace_buf + I->trace_buf_offset; T.cap = I->trace_buf_words; }
-
-    int32_t* q_pos = w.i32(Q_POS);
-    int32_t* q_rem = w.i32(Q_REM);
-    int32_t* q_full = w.i32(Q_FULL);
-    int32_t* q_inp = w.i32(Q_INP);
-    int64_t* q_arr = w.i64(Q_ARR);
-
-    int ai = 0;
-    int64_t next_arr = n > 0 ? arrival_of(Tarr, fac, 0) : SLOSIM_INF64;
-    int qh = 0, qt = 0;
-    int pf_k = 0;
-    int64_t pf_end = SLOSIM_INF64, pf_dur = 0;
-    int trn = 0;
-    int64_t tr_min = SLOSIM_INF64;
-    int ph = 0, pt = 0;
-    int an = 0;
-    int64_t amax = 0;        // max seq_len over the active set
-    int dc_prefix = -1;      // >= 0: the running batch is active[0, dc_prefix) (continuous); -1: flags
-    int64_t dc_end = SLOSIM_INF64, dc_dur = 0, dc_bsz = 0, dc_max = 0;
-    int64_t kv = 0;
-    int finished = 0;
-    int32_t c_ttft = 0, c_tpot = 0, c_e2e = 0, ntps = 0, max_q = 0, max_a = 0;
+    S.T = TraceW{nullptr, 0, 0};
+    if (FULL && S.B->trace_buf && I->trace_buf_offset >= 0) {
+        S.T.buf = S.B->trace_buf + I->trace_buf_offset;
+        S.T.cap = I->trace_buf_words;
+    }
+    S.ai = 0;
+    S.next_arr = S.n > 0 ? arrival_of(S.Tarr, S.fac, 0) : SLOSIM_INF64;
+    S.qh = S.qt = S.pf_k = S.trn = S.ph = S.pt = S.an = S.finished = 0;
+    S.pf_end = S.tr_min = S.dc_end = SLOSIM_INF64;
+    S.pf_dur = S.dc_dur = S.dc_bsz = S.dc_max = S.amax = S.kv = 0;
+    S.dc_prefix = -1;  // >= 0: the running batch is active[0, dc_prefix) (continuous); -1: flags
+    S.c_ttft = S.c_tpot = S.c_e2e = S.ntps = S.max_q = S.max_a = 0;
+    S.misses = S.worst_wait = S.psteps = S.dsteps = S.v_dec = S.b_dec = S.v_pre = S.t_end = 0;
+    S.D = 0;
     int32_t l_tpot = 0, l_e2e = 0;  // per-lane partial counts, reduced once at the end
     int64_t l_miss = 0;
-    int64_t misses = 0, worst_wait = 0, psteps = 0, dsteps = 0, v_dec = 0, b_dec = 0, v_pre = 0, t_end = 0;
-    uint64_t D = 0;
+    const int64_t tpot_slo = S.tpot_slo;
 
     for (;;) {
-        int64_t t = next_arr;
-        t = pf_end < t ? pf_end : t;
-        t = dc_end < t ? dc_end : t;
-        t = tr_min < t ? tr_min : t;
+        int64_t t = S.next_arr;
+        t = S.pf_end < t ? S.pf_end : t;
+        t = S.dc_end < t ? S.dc_end : t;
+        t = S.tr_min < t ? S.tr_min : t;
         if (t == SLOSIM_INF64) break;
-        t_end = t;
+        S.t_end = t;
 
-        // ---- arrivals (engine.py:288-291): a contiguous run of the trace
-        if (next_arr == t) {
-            for (;;) {
-                int p = ai + lane;
-                int64_t a = p < n ? arrival_of(Tarr, fac, p) : SLOSIM_INF64;
-                unsigned m = __ballot_sync(FULLMASK, a == t);
-                int cnt = __popc(m);
-                if (lane < cnt) {
-                    int qi = qt + lane;
-                    int32_t inp = Tinp[p];
-                    int32_t full = inp - Thit[p];
-                    q_pos[qi] = p; q_arr[qi] = a; q_inp[qi] = inp; q_full[qi] = full; q_rem[qi] = full;
-                    if (FULL && T.buf) {
-                        int64_t o = T.used + 3 * lane;
-                        T.put(o, SLOSIM_EV_ARRIVAL); T.put(o + 1, t); T.put(o + 2, p);
-                    }
-                }
-                T.used += 3 * cnt;
-                qt += cnt;
-                ai += cnt;
-                if (cnt < 32) { next_arr = __shfl_sync(FULLMASK, a, cnt); break; }
-            }
-            __syncwarp();
-        }
+        // rare events (a few per request) run out of line
+        if (S.next_arr == t) on_arrivals<FULL>(S, t, lane);
+        if (S.tr_min == t) on_transfers<FULL>(S, t, lane);
+        if (S.pf_end == t) on_prefill_done<FULL>(S, t, lane);
 
-        // ---- transfers due now that were pushed at earlier instants (engine.py:294-298)
-        if (tr_min == t) {
-            int64_t* tr_t = w.i64(TR_T);
-            int64_t* tr_tpf = w.i64(TR_TPF);
-            int32_t* tr_pos = w.i32(TR_POS);
-            int m_keep = 0;
-            for (int base = 0; base < trn; base += 32) {
-                int k = base + lane;
-                bool v = k < trn;
-                int64_t tt = v ? tr_t[k] : 0, tpf = v ? tr_tpf[k] : 0;
-                int32_t pos = v ? tr_pos[k] : 0;
-                bool due = v && tt == t;
-                unsigned dm = __ballot_sync(FULLMASK, due);
-                unsigned km = __ballot_sync(FULLMASK, v && !due);
-                __syncwarp();
-                if (v && !due) {
-                    int o = m_keep + __popc(km & lanemask_lt(lane));
-                    tr_t[o] = tt; tr_tpf[o] = tpf; tr_pos[o] = pos;
-                }
-                m_keep += __popc(km);
-                __syncwarp();
-                while (dm) {
-                    int j = __ffs((int)dm) - 1;
-                    dm &= dm - 1;
-                    int64_t jtpf = __shfl_sync(FULLMASK, tpf, j);
-                    int32_t jpos = __shfl_sync(FULLMASK, pos, j);
-                    pending_insert(w, ph, pt, jtpf, Tidr[jpos], t, jpos, lane);
-                    if (FULL && T.buf && lane == 0) { T.put(T.used, SLOSIM_EV_TRANSFER_DONE); T.put(T.used + 1, t); T.put(T.used + 2, jpos); }
-                    T.used += 3;
-                }
-            }
-            trn = m_keep;
-            int64_t mn = SLOSIM_INF64;
-            for (int k = lane; k < trn; k += 32) { int64_t tt = tr_t[k]; mn = tt < mn ? tt : mn; }
-            tr_min = wmin64(mn);
-        }
-
-        // ---- prefill step completion (engine.py:327-350)
-        if (pf_end == t) {
-            const int32_t* pf_qidx = w.i32(PF_QIDX);
-            const int32_t* pf_take = w.i32(PF_TAKE);
-            int64_t tot = 0;
-            uint64_t h = dstep(D, (uint64_t)t ^ 0xA5A5A5A5A5A5A5A5ULL);
-            if (FULL && T.buf && lane == 0) {
-                T.put(T.used, SLOSIM_EV_PREFILL_DONE); T.put(T.used + 1, t); T.put(T.used + 2, pf_dur); T.put(T.used + 3, pf_k);
-            }
-            T.used += 4;
-            int64_t tw_transfers = T.used + pf_k;  // delay-0 TransferDone records follow the batch list
-            int ncomp = 0, n0 = 0;
-            for (int base = 0; base < pf_k; base += 32) {
-                int e = base + lane;
-                bool v = e < pf_k;
-                int64_t take = 0;
-                int32_t pos = 0, inp = 0;
-                bool comp = false;
-                uint64_t word = 0;
-                if (v) {
-                    int qi = pf_qidx[e];
-                    take = pf_take[e];
-                    int32_t rem = q_rem[qi] - (int32_t)take;
-                    q_rem[qi] = rem;
-                    pos = q_pos[qi];
-                    inp = q_inp[qi];
-                    comp = rem == 0;
-                    word = ((uint64_t)(uint32_t)pos << 32) | (uint32_t)take;
-                    T.put(T.used + e, (int64_t)word);
-                }
-                tot += take;
-                // digest, batch order
-                int lim = pf_k - base < 32 ? pf_k - base : 32;
-                for (int j = 0; j < lim; j++) h = dstep(h, __shfl_sync(FULLMASK, word, j));
-                // completed requests leave the queue and start their KV transfer, batch order
-                int64_t delay = comp ? I->transfer_base_us + rint_i64(xmul((double)inp, I->transfer_per_token_us)) : 0;
-                unsigned cm = __ballot_sync(FULLMASK, comp);
-                unsigned zm = __ballot_sync(FULLMASK, comp && delay == 0);
-                if (FULL && T.buf && comp && delay == 0) {
-                    int64_t o = tw_transfers + 3 * (n0 + __popc(zm & lanemask_lt(lane)));
-                    T.put(o, SLOSIM_EV_TRANSFER_DONE); T.put(o + 1, t); T.put(o + 2, pos);
-                }
-                n0 += __popc(zm);
-                ncomp += __popc(cm);
-                if (FULL && rows && comp) B->rows.t_prefill_finish[row0 + pos] = t;
-                while (cm) {
-                    int j = __ffs((int)cm) - 1;
-                    cm &= cm - 1;
-                    int32_t jpos = __shfl_sync(FULLMASK, pos, j);
-                    int64_t jdel = __shfl_sync(FULLMASK, delay, j);
-                    if (jdel == 0) {
-                        pending_insert(w, ph, pt, t, Tidr[jpos], t, jpos, lane);
-                    } else {
-                        if (lane == 0) { w.i64(TR_T)[trn] = t + jdel; w.i64(TR_TPF)[trn] = t; w.i32(TR_POS)[trn] = jpos; }
-                        trn++;
-                        tr_min = t + jdel < tr_min ? t + jdel : tr_min;
-                    }
-                }
-            }
-            T.used += pf_k + 3 * n0;
-            tot = wsum64(tot);
-            est_tok += tot;
-            est_busy += pf_dur;
-            psteps++;
-            D = dstep(h, (uint64_t)pf_dur);
-            __syncwarp();
-            if (ppol == SLOSIM_PREFILL_FCFS) {
-                qh += ncomp;  // FCFS completes a prefix of the queue
-            } else if (ncomp) {
-                int o = qh;
-                for (int base = qh; base < qt; base += 32) {
-                    int qi = base + lane;
-                    bool v = qi < qt;
-                    int32_t pos = 0, rem = 0, full = 0, inp = 0;
-                    int64_t a = 0;
-                    if (v) { pos = q_pos[qi]; rem = q_rem[qi]; full = q_full[qi]; inp = q_inp[qi]; a = q_arr[qi]; }
-                    bool keep = v && rem > 0;
-                    unsigned km = __ballot_sync(FULLMASK, keep);
-                    __syncwarp();
-                    if (keep) {
-                        int d = o + __popc(km & lanemask_lt(lane));
-                        q_pos[d] = pos; q_rem[d] = rem; q_full[d] = full; q_inp[d] = inp; q_arr[d] = a;
-                    }
-                    o += __popc(km);
-                    __syncwarp();
-                }
-                qt = o;
-            }
-            pf_end = SLOSIM_INF64;
-        }
-
-        // ---- decode step completion (engine.py:394-413)
-        if (dc_end == t) {
+        // ---- decode step completion (engine.py:394-413): the hot path
+        if (S.dc_end == t) {
             int32_t* a_pos = w.i32(A_POS);
             int32_t* a_seq = w.i32(A_SEQ);
             int32_t* a_idr = w.i32(A_IDR);
@@ -673,8 +901,10 @@ __device__ __noinline__ void simulate(const Ctx& cx, int64_t ii, const WS& w, in
             uint32_t s = 0;
             int64_t kv_rel = 0, mx = 0;
             int o = 0;
-            int64_t tw0 = T.used + 5;
+            int64_t tw0 = S.T.used + 5;
             int nmem = 0;
+            const int an = S.an, dc_prefix = S.dc_prefix;
+#pragma unroll 1
             for (int base = 0; base < an; base += 32) {
                 int i = base + lane;
                 bool v = i < an;
@@ -700,29 +930,29 @@ __device__ __noinline__ void simulate(const Ctx& cx, int64_t ii, const WS& w, in
                         tpm = tpot <= (double)tpot_slo;
                         tps = xdiv((double)(outl - 1), xdiv((double)span, 1e6));
                         kv_rel += (int64_t)inp + outl;
-                        if (FULL && rows) {
+                        if (FULL && S.rows) {
                             bool ttm = (flag & 2) != 0;
-                            int64_t g = row0 + pos;
-                            B->rows.mean_tpot_us[g] = tpot;
-                            B->rows.decode_tps[g] = tps;
-                            B->rows.met_flags[g] = (uint8_t)((ttm ? 1 : 0) | (tpm ? 2 : 0) | ((ttm && tpm) ? 4 : 0));
-                            B->rows.deadline_misses[g] = miss;
-                            B->rows.t_last_token[g] = t;
+                            int64_t g = S.row0 + pos;
+                            S.B->rows.mean_tpot_us[g] = tpot;
+                            S.B->rows.decode_tps[g] = tps;
+                            S.B->rows.met_flags[g] = (uint8_t)((ttm ? 1 : 0) | (tpm ? 2 : 0) | ((ttm && tpm) ? 4 : 0));
+                            S.B->rows.deadline_misses[g] = miss;
+                            S.B->rows.t_last_token[g] = t;
                         }
                     }
                 }
                 unsigned rmask = __ballot_sync(FULLMASK, retire);
                 if (retire) {
-                    tps_buf[ntps + __popc(rmask & lanemask_lt(lane))] = tps;
+                    tps_buf[S.ntps + __popc(rmask & lanemask_lt(lane))] = tps;
                     l_miss += miss;
                     l_tpot += tpm;
                     l_e2e += tpm && (flag & 2);
                 }
-                ntps += __popc(rmask);
-                finished += __popc(rmask);
-                if (FULL && T.buf) {
+                S.ntps += __popc(rmask);
+                S.finished += __popc(rmask);
+                if (FULL && S.T.buf) {
                     unsigned bm = __ballot_sync(FULLMASK, inb);
-                    if (inb) T.put(tw0 + nmem + __popc(bm & lanemask_lt(lane)), pos);
+                    if (inb) S.T.put(tw0 + nmem + __popc(bm & lanemask_lt(lane)), pos);
                     nmem += __popc(bm);
                 }
                 // compact survivors (stable), clearing the in-batch bit
@@ -738,139 +968,47 @@ __device__ __noinline__ void simulate(const Ctx& cx, int64_t ii, const WS& w, in
                 o += __popc(km);
                 __syncwarp();
             }
-            an = o;
-            amax = __reduce_max_sync(FULLMASK, (int)mx);
+            S.an = o;
+            S.amax = __reduce_max_sync(FULLMASK, (int)mx);
             // retiring reservations: one REDUX when every lane's sum fits 26 bits
-            if (__all_sync(FULLMASK, kv_rel < (1LL << 26))) kv -= (int64_t)__reduce_add_sync(FULLMASK, (unsigned)kv_rel);
-            else kv -= wsum64(kv_rel);
+            if (__all_sync(FULLMASK, kv_rel < (1LL << 26))) S.kv -= (int64_t)__reduce_add_sync(FULLMASK, (unsigned)kv_rel);
+            else S.kv -= wsum64(kv_rel);
             s = __reduce_add_sync(FULLMASK, s);
             if (use_lut) {
-                if (lane == 0) lut_update(L, dc_bsz, dc_max, dc_dur);
+                if (lane == 0) lut_update(L, S.dc_bsz, S.dc_max, S.dc_dur);
                 __syncwarp();
             }
-            dsteps++;
-            D = dstep(D, (uint64_t)t ^ 0x5A5A5A5A5A5A5A5AULL);
-            D = dstep(D, ((uint64_t)s << 32) | (uint32_t)dc_bsz);
-            D = dstep(D, (uint64_t)dc_dur);
-            if (FULL && T.buf && lane == 0) {
-                T.put(T.used, SLOSIM_EV_DECODE_DONE); T.put(T.used + 1, t); T.put(T.used + 2, dc_dur);
-                T.put(T.used + 3, dc_bsz); T.put(T.used + 4, dc_max);
+            S.dsteps++;
+            S.D = dstep(S.D, (uint64_t)t ^ 0x5A5A5A5A5A5A5A5AULL);
+            S.D = dstep(S.D, ((uint64_t)s << 32) | (uint32_t)S.dc_bsz);
+            S.D = dstep(S.D, (uint64_t)S.dc_dur);
+            if (FULL && S.T.buf && lane == 0) {
+                S.T.put(S.T.used, SLOSIM_EV_DECODE_DONE); S.T.put(S.T.used + 1, t); S.T.put(S.T.used + 2, S.dc_dur);
+                S.T.put(S.T.used + 3, S.dc_bsz); S.T.put(S.T.used + 4, S.dc_max);
             }
-            T.used += 5 + (FULL && T.buf ? nmem : 0);
-            dc_end = SLOSIM_INF64;
+            S.T.used += 5 + (FULL && S.T.buf ? nmem : 0);
+            S.dc_end = SLOSIM_INF64;
         }
 
-        // ---- admission under the KV reservation (engine.py:355-375)
-        while (pt > ph) {
-            int k = ph + lane;
-            bool v = k < pt;
-            int32_t pos = v ? w.i32(PD_POS)[k] : 0;
-            int32_t outl = v ? Tout[pos] : 0, inp = v ? Tinp[pos] : 0;
-            int64_t need = (int64_t)inp + outl;
-            int64_t held = (v && outl > 1) ? need : 0;
-            int64_t excl = wscan_incl64(held, lane) - held;
-            bool ok = v && kv + excl + need <= kv_cap;
-            unsigned vm = __ballot_sync(FULLMASK, v);
-            unsigned okm = __ballot_sync(FULLMASK, ok);
-            unsigned fail = vm & ~okm;
-            int cnt = fail ? __ffs((int)fail) - 1 : __popc(vm);
-            bool adm = lane < cnt;
-            int64_t ttr = adm ? w.i64(PD_TTR)[k] : 0;
-            bool ttm = false;
-            if (adm) {
-                int64_t ttft = ttr - arrival_of(Tarr, fac, pos);
-                ttm = ttft <= ttft_slo;
-                if (FULL && T.buf) {
-                    int64_t o2 = T.used + 4 * lane;
-                    T.put(o2, SLOSIM_EV_ADMIT); T.put(o2 + 1, t); T.put(o2 + 2, pos); T.put(o2 + 3, ttr);
-                }
-                if (FULL && rows) {
-                    int64_t g = row0 + pos;
-                    B->rows.ttft_us[g] = ttft;
-                    B->rows.t_first_token[g] = ttr;
-                    if (outl == 1) {
-                        B->rows.mean_tpot_us[g] = 0.0;
-                        B->rows.decode_tps[g] = __longlong_as_double(0x7ff8000000000000LL);
-                        B->rows.met_flags[g] = (uint8_t)((ttm ? 1 : 0) | 2 | (ttm ? 4 : 0));
-                        B->rows.deadline_misses[g] = 0;
-                        B->rows.t_last_token[g] = ttr;
-                    }
-                }
-            }
-            T.used += 4 * cnt;
-            c_ttft += __popc(__ballot_sync(FULLMASK, adm && ttm));
-            unsigned one = __ballot_sync(FULLMASK, adm && outl == 1);
-            c_tpot += __popc(one);
-            c_e2e += __popc(__ballot_sync(FULLMASK, adm && outl == 1 && ttm));
-            finished += __popc(one);
-            unsigned dec = __ballot_sync(FULLMASK, adm && outl > 1);
-            if (adm && outl > 1) {
-                int d = an + __popc(dec & lanemask_lt(lane));
-                w.i32(A_POS)[d] = pos; w.i32(A_SEQ)[d] = inp; w.i32(A_IDR)[d] = w.i32(PD_IDR)[k];
-                w.i32(A_OUT)[d] = outl; w.i32(A_INP)[d] = inp; w.i32(A_MISS)[d] = 0; w.i64(A_TFIRST)[d] = ttr;
-                w.i32(A_FLAG)[d] = ttm ? 2 : 0;
-            }
-            an += __popc(dec);
-            amax = __reduce_max_sync(FULLMASK, (int)(adm && outl > 1 && inp > amax ? (int64_t)inp : amax));
-            kv += wsum64(adm ? held : 0);
-            ph += cnt;
-            __syncwarp();
-            if (cnt < 32) break;
-        }
+        if (S.pt > S.ph) on_admit<FULL>(S, t, lane);
+        if (S.pf_end == SLOSIM_INF64 && S.qt > S.qh) on_prefill_start<FULL>(S, t, lane);
 
-        // ---- start a prefill step (engine.py:307-325)
-        if (pf_end == SLOSIM_INF64 && qt > qh) {
-            int qlen = qt - qh;
-            v_pre += qlen;
-            max_q = qlen > max_q ? qlen : max_q;
-            pf_k = prefill_select(ppol, w, qh, qt, I->chunk_budget, t, est_tok, est_busy, ttft_slo, lane);
-            if (pf_k > 0) {
-                // ground-truth duration: ordered sum of curve increments (engine.py:175-183)
-                const int32_t* pf_qidx = w.i32(PF_QIDX);
-                const int32_t* pf_take = w.i32(PF_TAKE);
-                const int n_curve = P->n_curve;
-                double total = 0.0;
-                int64_t ww = 0;
-                for (int base = 0; base < pf_k; base += 32) {
-                    int e = base + lane;
-                    double term = 0.0;
-                    if (e < pf_k) {
-                        int qi = pf_qidx[e];
-                        int64_t take = pf_take[e];
-                        int64_t done = (int64_t)q_full[qi] - q_rem[qi];
-                        term = xsub(curve_at(n_curve, P->curve_x, P->curve_y, done + take),
-                                    curve_at(n_curve, P->curve_x, P->curve_y, done));
-                        if (done == 0) {  // first time scheduled (engine.py:322)
-                            int64_t wt = t - q_arr[qi];
-                            ww = wt > ww ? wt : ww;
-                            if (FULL && rows) B->rows.first_sched_us[row0 + q_pos[qi]] = t;
-                        }
-                    }
-                    int lim = pf_k - base < 32 ? pf_k - base : 32;
-                    for (int j = 0; j < lim; j++) total = xadd(total, __shfl_sync(FULLMASK, term, j));
-                }
-                ww = wmax64(ww);
-                worst_wait = ww > worst_wait ? ww : worst_wait;
-                int64_t d = rint_i64(total);
-                pf_dur = d < 1 ? 1 : d;
-                pf_end = t + pf_dur;
-            }
-        }
-
-        // ---- start a decode step (engine.py:377-392)
-        if (dc_end == SLOSIM_INF64 && an > 0) {
-            v_dec += an;
-            max_a = an > max_a ? an : max_a;
+        // ---- start a decode step (engine.py:377-392): the hot path
+        if (S.dc_end == SLOSIM_INF64 && S.an > 0) {
+            const int an = S.an;
+            S.v_dec += an;
+            S.max_a = an > S.max_a ? an : S.max_a;
             int bsz = an;
-            int64_t bmax = amax;
-            dc_prefix = an;
+            int64_t bmax = S.amax;
+            S.dc_prefix = an;
             if (DP == SLOSIM_DECODE_KAIROS_SLACK) {
                 // select_decode_batch decode_sched.py:60-111
                 const int32_t* a_seq = w.i32(A_SEQ);
                 const int32_t* a_inp = w.i32(A_INP);
                 const int64_t* a_tf = w.i64(A_TFIRST);
-                double fallback = lut_lookup(L, an, amax);
+                double fallback = lut_lookup(L, an, S.amax);
                 int64_t sl = SLOSIM_INF64;
+#pragma unroll 1
                 for (int i = lane; i < an; i += 32) {
                     int64_t ngen = (int64_t)a_seq[i] - a_inp[i];
                     int64_t v = tpot_slo * (ngen + 1) - (t - a_tf[i]);
@@ -883,62 +1021,23 @@ __device__ __noinline__ void simulate(const Ctx& cx, int64_t ii, const WS& w, in
                 int64_t ms;
                 int b = decode_scan(L, an, w.i32(A_ORD), a_seq, w.i32(A_FLAG), smin, &tcur, &ms, nullptr, nullptr,
                                     nullptr, nullptr, lane);
-                if (b > 0) { bsz = b; bmax = ms; dc_prefix = -1; }
+                if (b > 0) { bsz = b; bmax = ms; S.dc_prefix = -1; }
             }
-            b_dec += bsz;
+            S.b_dec += bsz;
             // _GroundTruth.decode_step_us engine.py:185-192
+            const slosim_profile_t* P = S.P;
             double val = P->gt_frozen ? lut_lookup(cx.frozen_tab + pid, bsz, bmax)
                                       : decode_formula(P->n_base, P->base_x, P->base_y, P->gamma, bsz, bmax);
             double eps = P->noise_eps;
             if (eps > 0) val = xmul(val, pcg_uniform(rng, xsub(1.0, eps), xadd(1.0, eps)));
             int64_t d = rint_i64(val);
-            dc_dur = d < 1 ? 1 : d;
-            dc_bsz = bsz;
-            dc_max = bmax;
-            dc_end = t + dc_dur;
+            S.dc_dur = d < 1 ? 1 : d;
+            S.dc_bsz = bsz;
+            S.dc_max = bmax;
+            S.dc_end = t + S.dc_dur;
         }
     }
-
-    // ---- finalize: aggregate (metrics.py:109-144)
-    double p50 = __longlong_as_double(0x7ff8000000000000LL), p90 = p50;
-    __syncwarp();
-    c_tpot += __reduce_add_sync(FULLMASK, (unsigned)l_tpot);
-    c_e2e += __reduce_add_sync(FULLMASK, (unsigned)l_e2e);
-    misses += wsum64(l_miss);
-    if (ntps > 0) {
-        int64_t r50 = (int64_t)ceil(xmul(50 / 100.0, (double)ntps));
-        int64_t r90 = (int64_t)ceil(xmul(90 / 100.0, (double)ntps));
-        p50 = radix_select(w.f64(TPS), ntps, r50 < 1 ? 1 : r50, lane);
-        p90 = radix_select(w.f64(TPS), ntps, r90 < 1 ? 1 : r90, lane);
-    }
-    if (FULL && (B->flags & SLOSIM_F_EXPORT_LUT) && B->lut_out_sums) {
-        const int FR = LUT_CELLS;
-        const int nb = P->nb, ns = P->ns;
-        for (int c = lane; c < FR; c += 32) {
-            int i = c / SLOSIM_MAX_SEQ_BUCKETS, j = c % SLOSIM_MAX_SEQ_BUCKETS;
-            bool in = i < nb && j < ns;
-            B->lut_out_sums[ii * FR + c] = in ? L->sum[i * ns + j] : 0.0;
-            B->lut_out_counts[ii * FR + c] = in ? L->cnt[i * ns + j] : 0;
-        }
-    }
-    if (FULL && T.buf && lane == 0 && T.used + 2 <= T.cap) { T.buf[T.used] = SLOSIM_EV_END; T.buf[T.used + 1] = T.used + 2; }
-    if (lane == 0) {
-        slosim_summary_t s;
-        s.status = (finished == n ? SLOSIM_OK : -1) | ((FULL && T.buf && T.used + 2 > T.cap) ? 0x100 : 0);
-        s.n = n;
-        s.ttft_met = c_ttft; s.tpot_met = c_tpot; s.e2e_met = c_e2e; s.n_tps = ntps;
-        s.tps_p50 = p50; s.tps_p90 = p90;
-        s.worst_queue_wait_us = worst_wait;
-        s.prefill_steps = psteps; s.decode_steps = dsteps;
-        s.digest = D;
-        s.v_dec = v_dec; s.b_dec = b_dec; s.v_pre = v_pre;
-        s.deadline_misses = misses;
-        s.t_end_us = t_end;
-        s.est_tokens = est_tok; s.est_busy_us = est_busy;
-        s.max_queue = max_q; s.max_active = max_a;
-        s.sim_cycles = clock64() - c0;
-        B->summaries[ii] = s;
-    }
+    on_finalize<FULL>(S, l_tpot, l_e2e, l_miss, c0, lane);
 }
 
 #ifndef SLOSIM_MIN_BLOCKS

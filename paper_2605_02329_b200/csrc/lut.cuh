@@ -52,13 +52,15 @@ __device__ __forceinline__ int bucket_index(const int32_t* a, int n, int64_t x) 
     return i < n - 1 ? i : n - 1;
 }
 
+__device__ __noinline__ int bisect_left_call(const int32_t* a, int n, int64_t x) { return bisect_left(a, n, x); }
+
 __device__ __forceinline__ int lut_bidx(const LutMem* L, int64_t b) {
-    return (b >= 0 && b <= 256) ? (int)L->bidx[b] : bisect_left(L->bb, L->nb, b);
+    return (b >= 0 && b <= 256) ? (int)L->bidx[b] : bisect_left_call(L->bb, L->nb, b);
 }
 
 __device__ __forceinline__ int lut_sidx(const LutMem* L, int64_t s) {
     int64_t q = s >> L->sshift;
-    if (q < 0 || q > 256) return bisect_left(L->sb, L->ns, s);
+    if (q < 0 || q > 256) return bisect_left_call(L->sb, L->ns, s);
     int j = L->sidx[q];
     while (j < L->ns && (int64_t)L->sb[j] < s) j++;
     return j;
@@ -130,6 +132,7 @@ __device__ void lut_build(LutMem* L, int nb, int ns, const int32_t* bb, const in
 // Copy of a built LutMem (only the live part of the frame).
 __device__ void lut_copy(LutMem* dst, const LutMem* src, int lane) {
     int K = src->nb * src->ns;
+#pragma unroll 1
     for (int c = lane; c < K; c += 32) {
         dst->sum[c] = src->sum[c]; dst->mean[c] = src->mean[c]; dst->slope[c] = src->slope[c]; dst->cnt[c] = src->cnt[c];
     }
@@ -211,9 +214,8 @@ __device__ __forceinline__ double lut_row_eval(const LutMem* L, int r, int64_t s
     return xadd(xmul(L->slope[c + jp], xsub((double)seq, (double)L->sb[jp])), L->mean[c + jp]);
 }
 
-// DecodeStepLUT.lookup costmodel.py:157-187 (bsz, seq >= 1; LUT non-empty).
-__device__ __forceinline__ double lut_lookup(const LutMem* L, int64_t bsz, int64_t seq) {
-    if (L->full) return lut_eval(L, lut_rows(L, bsz), lut_col(L, seq));
+// DecodeStepLUT.lookup costmodel.py:157-187, general path (some cells unpopulated).
+__device__ __noinline__ double lut_lookup_general(const LutMem* L, int64_t bsz, int64_t seq) {
     int i = lut_bidx(L, bsz);
     int j0 = lut_sidx(L, seq);
     int nb = L->nb, ns = L->ns;
@@ -232,9 +234,18 @@ __device__ __forceinline__ double lut_lookup(const LutMem* L, int64_t bsz, int64
     return xadd(vlo, xdiv(xmul(xsub(vhi, vlo), (double)(bsz - L->bb[rlo])), (double)(L->bb[rhi] - L->bb[rlo])));
 }
 
+// DecodeStepLUT.lookup costmodel.py:157-187 (bsz, seq >= 1; LUT non-empty).
+__device__ __forceinline__ double lut_lookup(const LutMem* L, int64_t bsz, int64_t seq) {
+    if (L->full) return lut_eval(L, lut_rows(L, bsz), lut_col(L, seq));
+    return lut_lookup_general(L, bsz, seq);
+}
+
 // DecodeStepLUT.update costmodel.py:118-128 (single thread; caller syncs the warp).
 __device__ void lut_update(LutMem* L, int64_t bsz, int64_t max_seq, int64_t obs) {
-    int i = bucket_index(L->bb, L->nb, bsz), j = bucket_index(L->sb, L->ns, max_seq);
+    // _bucket_index: smallest bucket >= key, clamped to the last (table lookups)
+    int i = lut_bidx(L, bsz), j = lut_sidx(L, max_seq);
+    i = i < L->nb - 1 ? i : L->nb - 1;
+    j = j < L->ns - 1 ? j : L->ns - 1;
     int c = i * L->ns + j;
     bool fresh = L->cnt[c] == 0;
     L->sum[c] = xadd(L->sum[c], (double)obs);
