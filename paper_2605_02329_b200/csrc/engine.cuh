@@ -479,12 +479,60 @@ struct Sim {
     // event state
     int ai, qh, qt, pf_k, trn, ph, pt, an, dc_prefix, finished;
     int64_t next_arr, pf_end, pf_dur, tr_min, dc_end, dc_dur, dc_bsz, dc_max, amax, kv, est_tok, est_busy;
-    // counters
-    int32_t c_ttft, c_tpot, c_e2e, ntps, max_q, max_a;
-    int64_t misses, worst_wait, psteps, dsteps, v_dec, b_dec, v_pre, t_end;
+    // active-set representation: register slots (lane i holds slot i, occupancy
+    // mask `amask`, running batch `dc_mask`) while <= 32 requests are active,
+    // the workspace arrays (A_*) otherwise
+    bool regmode;
+    uint32_t amask, dc_mask;
+    // counters (l_*: per-lane partials, reduced at the end)
+    int32_t c_ttft, c_tpot, c_e2e, ntps, max_q, max_a, l_tpot, l_e2e;
+    int64_t misses, worst_wait, psteps, dsteps, v_dec, b_dec, v_pre, t_end, l_miss;
     uint64_t D;
     TraceW T;
 };
+
+// One active decode request held in a lane's registers (engine.py:374 _active).
+struct Slot {
+    int32_t pos, seq, idr, out, inp, miss, flag;  // flag bit1: TTFT met
+    int64_t tf;                                   // t_first_token
+};
+
+// 64-bit signed warp minimum from two 32-bit REDUX operations.
+__device__ __forceinline__ int64_t wmin64_redux(int64_t v) {
+    int hi = (int)(v >> 32);
+    int mh = __reduce_min_sync(FULLMASK, hi);
+    unsigned lo = hi == mh ? (unsigned)(uint64_t)v : 0xffffffffu;
+    unsigned ml = __reduce_min_sync(FULLMASK, lo);
+    return (int64_t)(((uint64_t)(uint32_t)mh << 32) | ml);
+}
+
+// register slots -> workspace arrays (compacted, slot order); running-batch membership
+// moves to the flag bit0 representation of memory mode
+__device__ __noinline__ void to_memory_mode(Sim& S, Slot& sl, int lane) {
+    bool occ = (S.amask >> lane) & 1u;
+    int d = __popc(S.amask & lanemask_lt(lane));
+    if (occ) {
+        S.w.i32(A_POS)[d] = sl.pos; S.w.i32(A_SEQ)[d] = sl.seq; S.w.i32(A_IDR)[d] = sl.idr; S.w.i32(A_OUT)[d] = sl.out;
+        S.w.i32(A_INP)[d] = sl.inp; S.w.i32(A_MISS)[d] = sl.miss; S.w.i64(A_TFIRST)[d] = sl.tf;
+        S.w.i32(A_FLAG)[d] = (sl.flag & 2) | (int)((S.dc_mask >> lane) & 1u);
+    }
+    __syncwarp();
+    S.an = __popc(S.amask);
+    S.dc_prefix = -1;
+    S.regmode = false;
+}
+
+// workspace arrays -> register slots (when <= 32 are active and no decode step is running)
+__device__ __noinline__ void to_register_mode(Sim& S, Slot& sl, int lane) {
+    if (lane < S.an) {
+        sl.pos = S.w.i32(A_POS)[lane]; sl.seq = S.w.i32(A_SEQ)[lane]; sl.idr = S.w.i32(A_IDR)[lane];
+        sl.out = S.w.i32(A_OUT)[lane]; sl.inp = S.w.i32(A_INP)[lane]; sl.miss = S.w.i32(A_MISS)[lane];
+        sl.flag = S.w.i32(A_FLAG)[lane] & 2; sl.tf = S.w.i64(A_TFIRST)[lane];
+    }
+    S.amask = S.an >= 32 ? 0xffffffffu : ((1u << S.an) - 1u);
+    S.dc_mask = 0;
+    S.regmode = true;
+}
 
 // ---- arrivals (engine.py:288-291): a contiguous run of the trace
 template <bool FULL>
@@ -658,7 +706,7 @@ __device__ __noinline__ void on_prefill_done(Sim& S, int64_t t, int lane) {
 
 // ---- admission under the KV reservation (engine.py:355-375)
 template <bool FULL>
-__device__ __noinline__ void on_admit(Sim& S, int64_t t, int lane) {
+__device__ __noinline__ void on_admit(Sim& S, Slot& sl, int64_t t, int lane) {
     const slosim_batch_t* B = S.B;
     while (S.pt > S.ph) {
         int k = S.ph + lane;
@@ -675,6 +723,7 @@ __device__ __noinline__ void on_admit(Sim& S, int64_t t, int lane) {
         int cnt = fail ? __ffs((int)fail) - 1 : __popc(vm);
         bool adm = lane < cnt;
         int64_t ttr = adm ? S.w.i64(PD_TTR)[k] : 0;
+        int32_t idr = adm ? S.w.i32(PD_IDR)[k] : 0;
         bool ttm = false;
         if (adm) {
             int64_t ttft = ttr - arrival_of(S.Tarr, S.fac, pos);
@@ -703,13 +752,33 @@ __device__ __noinline__ void on_admit(Sim& S, int64_t t, int lane) {
         S.c_e2e += __popc(__ballot_sync(FULLMASK, adm && outl == 1 && ttm));
         S.finished += __popc(one);
         unsigned dec = __ballot_sync(FULLMASK, adm && outl > 1);
-        if (adm && outl > 1) {
-            int d = S.an + __popc(dec & lanemask_lt(lane));
-            S.w.i32(A_POS)[d] = pos; S.w.i32(A_SEQ)[d] = inp; S.w.i32(A_IDR)[d] = S.w.i32(PD_IDR)[k];
-            S.w.i32(A_OUT)[d] = outl; S.w.i32(A_INP)[d] = inp; S.w.i32(A_MISS)[d] = 0; S.w.i64(A_TFIRST)[d] = ttr;
-            S.w.i32(A_FLAG)[d] = ttm ? 2 : 0;
+        int ndec = __popc(dec);
+        if (S.regmode && __popc(S.amask) + ndec > 32) to_memory_mode(S, sl, lane);
+        if (S.regmode) {
+            // the r-th admitted decoding request takes the r-th lowest free slot
+            unsigned freem = ~S.amask;
+            int fr = __popc(freem & lanemask_lt(lane));
+            bool take = ((freem >> lane) & 1u) && fr < ndec;
+            int src = ndec ? (int)__fns(dec, 0, (fr < ndec ? fr : 0) + 1) : 0;
+            int32_t npos = __shfl_sync(FULLMASK, pos, src), ninp = __shfl_sync(FULLMASK, inp, src);
+            int32_t nout = __shfl_sync(FULLMASK, outl, src), nidr = __shfl_sync(FULLMASK, idr, src);
+            int64_t ntf = __shfl_sync(FULLMASK, ttr, src);
+            bool nttm = __shfl_sync(FULLMASK, ttm, src);
+            if (take) {
+                sl.pos = npos; sl.seq = ninp; sl.idr = nidr; sl.out = nout; sl.inp = ninp; sl.miss = 0;
+                sl.flag = nttm ? 2 : 0; sl.tf = ntf;
+            }
+            S.amask |= __ballot_sync(FULLMASK, take);
+            S.an = __popc(S.amask);
+        } else {
+            if (adm && outl > 1) {
+                int d = S.an + __popc(dec & lanemask_lt(lane));
+                S.w.i32(A_POS)[d] = pos; S.w.i32(A_SEQ)[d] = inp; S.w.i32(A_IDR)[d] = idr;
+                S.w.i32(A_OUT)[d] = outl; S.w.i32(A_INP)[d] = inp; S.w.i32(A_MISS)[d] = 0; S.w.i64(A_TFIRST)[d] = ttr;
+                S.w.i32(A_FLAG)[d] = ttm ? 2 : 0;
+            }
+            S.an += ndec;
         }
-        S.an += __popc(dec);
         S.amax = __reduce_max_sync(FULLMASK, (int)(adm && outl > 1 && inp > S.amax ? (int64_t)inp : S.amax));
         S.kv += wsum64(adm ? held : 0);
         S.ph += cnt;
@@ -763,13 +832,13 @@ __device__ __noinline__ void on_prefill_start(Sim& S, int64_t t, int lane) {
 
 // ---- finalize: aggregate (metrics.py:109-144)
 template <bool FULL>
-__device__ __noinline__ void on_finalize(Sim& S, int32_t l_tpot, int32_t l_e2e, int64_t l_miss, long long c0, int lane) {
+__device__ __noinline__ void on_finalize(Sim& S, long long c0, int lane) {
     const slosim_batch_t* B = S.B;
     double p50 = __longlong_as_double(0x7ff8000000000000LL), p90 = p50;
     __syncwarp();
-    S.c_tpot += __reduce_add_sync(FULLMASK, (unsigned)l_tpot);
-    S.c_e2e += __reduce_add_sync(FULLMASK, (unsigned)l_e2e);
-    S.misses += wsum64(l_miss);
+    S.c_tpot += __reduce_add_sync(FULLMASK, (unsigned)S.l_tpot);
+    S.c_e2e += __reduce_add_sync(FULLMASK, (unsigned)S.l_e2e);
+    S.misses += wsum64(S.l_miss);
     if (S.ntps > 0) {
         int64_t r50 = (int64_t)ceil(xmul(50 / 100.0, (double)S.ntps));
         int64_t r90 = (int64_t)ceil(xmul(90 / 100.0, (double)S.ntps));
@@ -805,6 +874,187 @@ __device__ __noinline__ void on_finalize(Sim& S, int32_t l_tpot, int32_t l_e2e, 
         s.sim_cycles = clock64() - c0;
         B->summaries[S.ii] = s;
     }
+}
+
+// ---- memory-mode decode step completion (> 32 active; engine.py:394-413)
+template <bool FULL>
+__device__ __noinline__ void on_decode_done_mem(Sim& S, Slot& sl, int64_t t, uint32_t& s_out, int& nmem_out,
+                                               int lane) {
+    const WS& w = S.w;
+    int32_t* a_pos = w.i32(A_POS);
+    int32_t* a_seq = w.i32(A_SEQ);
+    int32_t* a_idr = w.i32(A_IDR);
+    int32_t* a_out = w.i32(A_OUT);
+    int32_t* a_inp = w.i32(A_INP);
+    int32_t* a_miss = w.i32(A_MISS);
+    int32_t* a_flag = w.i32(A_FLAG);
+    int64_t* a_tf = w.i64(A_TFIRST);
+    double* tps_buf = w.f64(TPS);
+    uint32_t s = 0;
+    int64_t kv_rel = 0, mx = 0;
+    int o = 0;
+    int64_t tw0 = S.T.used + 5;
+    int nmem = 0;
+    const int an = S.an, dc_prefix = S.dc_prefix;
+    const int64_t tpot_slo = S.tpot_slo;
+    for (int base = 0; base < an; base += 32) {
+        int i = base + lane;
+        bool v = i < an;
+        int32_t flag = 0, pos = 0, seq = 0, idr = 0, outl = 0, inp = 0, miss = 0;
+        int64_t tf = 0;
+        if (v) {
+            flag = a_flag[i]; pos = a_pos[i]; seq = a_seq[i]; idr = a_idr[i]; outl = a_out[i]; inp = a_inp[i];
+            miss = a_miss[i]; tf = a_tf[i];
+        }
+        bool inb = v && (dc_prefix >= 0 ? i < dc_prefix : (flag & 1));
+        bool retire = false, tpm = false;
+        double tps = 0.0;
+        if (inb) {
+            seq += 1;
+            int64_t ngen = seq - inp;
+            s += member_hash((uint32_t)pos);
+            if (t > tf + ngen * tpot_slo) miss++;  // deadline_misses metrics.py:57-69
+            if (ngen == outl - 1) {
+                retire = true;
+                int64_t span = t - tf;
+                double tpot = idiv(span, (int64_t)(outl - 1));
+                tpm = tpot <= (double)tpot_slo;
+                tps = xdiv((double)(outl - 1), xdiv((double)span, 1e6));
+                kv_rel += (int64_t)inp + outl;
+                if (FULL && S.rows) {
+                    bool ttm = (flag & 2) != 0;
+                    int64_t g = S.row0 + pos;
+                    S.B->rows.mean_tpot_us[g] = tpot;
+                    S.B->rows.decode_tps[g] = tps;
+                    S.B->rows.met_flags[g] = (uint8_t)((ttm ? 1 : 0) | (tpm ? 2 : 0) | ((ttm && tpm) ? 4 : 0));
+                    S.B->rows.deadline_misses[g] = miss;
+                    S.B->rows.t_last_token[g] = t;
+                }
+            }
+        }
+        unsigned rmask = __ballot_sync(FULLMASK, retire);
+        if (retire) {
+            tps_buf[S.ntps + __popc(rmask & lanemask_lt(lane))] = tps;
+            S.l_miss += miss;
+            S.l_tpot += tpm;
+            S.l_e2e += tpm && (flag & 2);
+        }
+        S.ntps += __popc(rmask);
+        S.finished += __popc(rmask);
+        if (FULL && S.T.buf) {
+            unsigned bm = __ballot_sync(FULLMASK, inb);
+            if (inb) S.T.put(tw0 + nmem + __popc(bm & lanemask_lt(lane)), pos);
+            nmem += __popc(bm);
+        }
+        bool keep = v && !retire;
+        unsigned km = __ballot_sync(FULLMASK, keep);
+        __syncwarp();
+        if (keep) {
+            int d = o + __popc(km & lanemask_lt(lane));
+            a_pos[d] = pos; a_seq[d] = seq; a_idr[d] = idr; a_out[d] = outl; a_inp[d] = inp;
+            a_miss[d] = miss; a_tf[d] = tf; a_flag[d] = flag & ~1;
+            mx = seq > mx ? seq : mx;
+        }
+        o += __popc(km);
+        __syncwarp();
+    }
+    S.an = o;
+    S.amax = __reduce_max_sync(FULLMASK, (int)mx);
+    S.kv -= wsum64(kv_rel);
+    s_out = __reduce_add_sync(FULLMASK, s);
+    nmem_out = nmem;
+    if (S.an <= 32) to_register_mode(S, sl, lane);
+}
+
+// ---- memory-mode decode start (> 32 active; engine.py:377-392, decode_sched.py:60-124)
+template <int DP>
+__device__ __noinline__ void on_decode_start_mem(Sim& S, int64_t t, int& bsz, int64_t& bmax, int lane) {
+    const WS& w = S.w;
+    const int an = S.an;
+    bsz = an;
+    bmax = S.amax;
+    S.dc_prefix = an;
+    if (DP == SLOSIM_DECODE_KAIROS_SLACK) {
+        const int32_t* a_seq = w.i32(A_SEQ);
+        const int32_t* a_inp = w.i32(A_INP);
+        const int64_t* a_tf = w.i64(A_TFIRST);
+        double fallback = lut_lookup(S.L, an, S.amax);
+        int64_t sl = SLOSIM_INF64;
+        for (int i = lane; i < an; i += 32) {
+            int64_t ngen = (int64_t)a_seq[i] - a_inp[i];
+            int64_t v = S.tpot_slo * (ngen + 1) - (t - a_tf[i]);
+            sl = v < sl ? v : sl;
+        }
+        sl = wmin64(sl);
+        double smin = xsub((double)sl, fallback);
+        decode_order(an, a_seq, w.i32(A_IDR), w.i32(A_ORD), lane);
+        double tcur;
+        int64_t ms;
+        int b = decode_scan(S.L, an, w.i32(A_ORD), a_seq, w.i32(A_FLAG), smin, &tcur, &ms, nullptr, nullptr, nullptr,
+                            nullptr, lane);
+        if (b > 0) { bsz = b; bmax = ms; S.dc_prefix = -1; }
+    }
+}
+
+// Alg. 3 (select_decode_batch decode_sched.py:60-111) on register slots, fully
+// populated LUT: dual-hypothesis rounds in rank space.  Lane i knows the rank
+// of its slot in (seq_len, id) order and the lane of its rank predecessor.
+// X: all candidates from rank s on are admitted (|B| = b + rank - s); the lowest
+// failing rank ends the admitted run.  If rank s itself fails, Y tests the rest
+// with the unchanged (|B|, t_cur) and admits the lowest admissible rank.
+// Returns |B| (0 = fallback) and the admitted slot mask.
+__device__ __forceinline__ int scan_slots(const LutMem* L, uint32_t amask, int an, const Slot& sl, double smin,
+                                          uint32_t& adm, int64_t& mseq, int lane) {
+    bool occ = (amask >> lane) & 1u;
+    uint64_t key = occ ? (((uint64_t)(uint32_t)sl.seq << 32) | (uint32_t)sl.idr) : ~0ULL;
+    int rank = 0, pred = lane;
+    uint64_t best = 0;
+    for (uint32_t m = amask; m; m &= m - 1) {
+        int j = __ffs((int)m) - 1;
+        uint64_t kj = __shfl_sync(FULLMASK, key, j);
+        if (kj < key) {
+            rank++;
+            if (kj >= best) { best = kj; pred = j; }
+        }
+    }
+    ColSel cs = lut_col(L, occ ? sl.seq : 1);
+    int b = 0, s = 0;
+    double tcur = 0.0;
+    adm = 0;
+    mseq = 0;
+    while (s < an) {
+        bool valid = occ && rank >= s;
+        int64_t bx = b + (rank - s) + 1;
+        double x = valid ? lut_eval(L, lut_rows_nb(L, bx), cs) : 0.0;
+        double xprev = __shfl_sync(FULLMASK, x, pred);
+        double tprev = rank == s ? tcur : xprev;
+        int64_t bprev = bx - 1;
+        bool okx = valid && x <= smin && (bprev == 0 || xdiv((double)(bprev + 1), x) > xdiv((double)bprev, tprev));
+        int f = __reduce_min_sync(FULLMASK, (valid && !okx) ? rank : an);
+        adm |= __ballot_sync(FULLMASK, valid && rank < f);
+        if (f > s) {
+            int lf = __ffs((int)__ballot_sync(FULLMASK, occ && rank == f - 1)) - 1;
+            tcur = __shfl_sync(FULLMASK, x, lf);
+            mseq = __shfl_sync(FULLMASK, sl.seq, lf);
+            b += f - s;
+            s = f + 1;  // rank f is rejected under the now-current state
+            continue;
+        }
+        RowSel rs = lut_rows(L, b + 1);
+        double thr = b ? xdiv((double)b, tcur) : 0.0;
+        bool vy = occ && rank > s;
+        double y = vy ? lut_eval(L, rs, cs) : 0.0;
+        bool oky = vy && y <= smin && (b == 0 || xdiv((double)(b + 1), y) > thr);
+        int g = __reduce_min_sync(FULLMASK, oky ? rank : an);
+        if (g >= an) break;
+        int lg = __ffs((int)__ballot_sync(FULLMASK, occ && rank == g)) - 1;
+        adm |= 1u << lg;
+        tcur = __shfl_sync(FULLMASK, y, lg);
+        mseq = __shfl_sync(FULLMASK, sl.seq, lg);
+        b++;
+        s = g + 1;
+    }
+    return b;
 }
 
 // DP: decode policy (compile-time), FULL: event trace / per-request rows / LUT
@@ -866,164 +1116,180 @@ __device__ __noinline__ void simulate(const Ctx& cx, int64_t ii, const WS& w, in
     S.qh = S.qt = S.pf_k = S.trn = S.ph = S.pt = S.an = S.finished = 0;
     S.pf_end = S.tr_min = S.dc_end = SLOSIM_INF64;
     S.pf_dur = S.dc_dur = S.dc_bsz = S.dc_max = S.amax = S.kv = 0;
-    S.dc_prefix = -1;  // >= 0: the running batch is active[0, dc_prefix) (continuous); -1: flags
-    S.c_ttft = S.c_tpot = S.c_e2e = S.ntps = S.max_q = S.max_a = 0;
-    S.misses = S.worst_wait = S.psteps = S.dsteps = S.v_dec = S.b_dec = S.v_pre = S.t_end = 0;
+    S.dc_prefix = -1;
+    S.regmode = true;
+    S.amask = S.dc_mask = 0;
+    S.c_ttft = S.c_tpot = S.c_e2e = S.ntps = S.max_q = S.max_a = S.l_tpot = S.l_e2e = 0;
+    S.misses = S.worst_wait = S.psteps = S.dsteps = S.v_dec = S.b_dec = S.v_pre = S.t_end = S.l_miss = 0;
     S.D = 0;
-    int32_t l_tpot = 0, l_e2e = 0;  // per-lane partial counts, reduced once at the end
-    int64_t l_miss = 0;
+    Slot sl{0, 0, 0, 0, 0, 0, 0, 0};
     const int64_t tpot_slo = S.tpot_slo;
+    double* tps_buf = w.f64(TPS);
+
+    // hot state in registers; synced with S around the (rare) out-of-line calls
+    int64_t next_arr, pf_end, dc_end, tr_min, dc_dur, dc_bsz, dc_max, amax, kv, t_end = 0;
+    int an, ph, pt, qh, qt, ntps, finished;
+    uint32_t amask, dc_mask;
+    bool regmode;
+    uint64_t D;
+    int64_t dsteps = 0, v_dec = 0, b_dec = 0;
+    int32_t max_a = 0;
+#define SIM_SYNC_IN()                                                                                          \
+    next_arr = S.next_arr; pf_end = S.pf_end; dc_end = S.dc_end; tr_min = S.tr_min; dc_dur = S.dc_dur;       \
+    dc_bsz = S.dc_bsz; dc_max = S.dc_max; amax = S.amax; kv = S.kv; an = S.an; ph = S.ph; pt = S.pt;          \
+    qh = S.qh; qt = S.qt; ntps = S.ntps; finished = S.finished; amask = S.amask; dc_mask = S.dc_mask;          \
+    regmode = S.regmode; D = S.D
+#define SIM_SYNC_OUT()                                                                                         \
+    S.next_arr = next_arr; S.pf_end = pf_end; S.dc_end = dc_end; S.tr_min = tr_min; S.dc_dur = dc_dur;       \
+    S.dc_bsz = dc_bsz; S.dc_max = dc_max; S.amax = amax; S.kv = kv; S.an = an; S.ph = ph; S.pt = pt;          \
+    S.qh = qh; S.qt = qt; S.ntps = ntps; S.finished = finished; S.amask = amask; S.dc_mask = dc_mask;          \
+    S.regmode = regmode; S.D = D
+    SIM_SYNC_IN();
 
     for (;;) {
-        int64_t t = S.next_arr;
-        t = S.pf_end < t ? S.pf_end : t;
-        t = S.dc_end < t ? S.dc_end : t;
-        t = S.tr_min < t ? S.tr_min : t;
+        int64_t t = next_arr;
+        t = pf_end < t ? pf_end : t;
+        t = dc_end < t ? dc_end : t;
+        t = tr_min < t ? tr_min : t;
         if (t == SLOSIM_INF64) break;
-        S.t_end = t;
+        t_end = t;
 
-        // rare events (a few per request) run out of line
-        if (S.next_arr == t) on_arrivals<FULL>(S, t, lane);
-        if (S.tr_min == t) on_transfers<FULL>(S, t, lane);
-        if (S.pf_end == t) on_prefill_done<FULL>(S, t, lane);
+        // rare events (a few per request) run out of line, in the reference's order
+        if (next_arr == t || tr_min == t || pf_end == t) {
+            SIM_SYNC_OUT();
+            if (S.next_arr == t) on_arrivals<FULL>(S, t, lane);
+            if (S.tr_min == t) on_transfers<FULL>(S, t, lane);
+            if (S.pf_end == t) on_prefill_done<FULL>(S, t, lane);
+            SIM_SYNC_IN();
+        }
 
         // ---- decode step completion (engine.py:394-413): the hot path
-        if (S.dc_end == t) {
-            int32_t* a_pos = w.i32(A_POS);
-            int32_t* a_seq = w.i32(A_SEQ);
-            int32_t* a_idr = w.i32(A_IDR);
-            int32_t* a_out = w.i32(A_OUT);
-            int32_t* a_inp = w.i32(A_INP);
-            int32_t* a_miss = w.i32(A_MISS);
-            int32_t* a_flag = w.i32(A_FLAG);
-            int64_t* a_tf = w.i64(A_TFIRST);
-            double* tps_buf = w.f64(TPS);
+        if (dc_end == t) {
             uint32_t s = 0;
-            int64_t kv_rel = 0, mx = 0;
-            int o = 0;
-            int64_t tw0 = S.T.used + 5;
             int nmem = 0;
-            const int an = S.an, dc_prefix = S.dc_prefix;
-#pragma unroll 1
-            for (int base = 0; base < an; base += 32) {
-                int i = base + lane;
-                bool v = i < an;
-                int32_t flag = 0, pos = 0, seq = 0, idr = 0, outl = 0, inp = 0, miss = 0;
-                int64_t tf = 0;
-                if (v) {
-                    flag = a_flag[i]; pos = a_pos[i]; seq = a_seq[i]; idr = a_idr[i]; outl = a_out[i]; inp = a_inp[i];
-                    miss = a_miss[i]; tf = a_tf[i];
-                }
-                bool inb = v && (dc_prefix >= 0 ? i < dc_prefix : (flag & 1));
+            if (regmode) {
+                bool inb = (dc_mask >> lane) & 1u;
                 bool retire = false, tpm = false;
                 double tps = 0.0;
+                int64_t kv_rel = 0;
+                uint32_t hsh = 0;
                 if (inb) {
-                    seq += 1;
-                    int64_t ngen = seq - inp;
-                    s += member_hash((uint32_t)pos);
-                    if (t > tf + ngen * tpot_slo) miss++;  // deadline_misses metrics.py:57-69
-                    if (ngen == outl - 1) {
+                    sl.seq += 1;
+                    int64_t ngen = sl.seq - sl.inp;
+                    hsh = member_hash((uint32_t)sl.pos);
+                    if (t > sl.tf + ngen * tpot_slo) sl.miss++;  // deadline_misses metrics.py:57-69
+                    if (ngen == sl.out - 1) {
                         // request_metrics metrics.py:72-84 at retirement
                         retire = true;
-                        int64_t span = t - tf;
-                        double tpot = idiv(span, (int64_t)(outl - 1));
+                        int64_t span = t - sl.tf;
+                        double tpot = idiv(span, (int64_t)(sl.out - 1));
                         tpm = tpot <= (double)tpot_slo;
-                        tps = xdiv((double)(outl - 1), xdiv((double)span, 1e6));
-                        kv_rel += (int64_t)inp + outl;
+                        tps = xdiv((double)(sl.out - 1), xdiv((double)span, 1e6));
+                        kv_rel = (int64_t)sl.inp + sl.out;
                         if (FULL && S.rows) {
-                            bool ttm = (flag & 2) != 0;
-                            int64_t g = S.row0 + pos;
+                            bool ttm = (sl.flag & 2) != 0;
+                            int64_t g = S.row0 + sl.pos;
                             S.B->rows.mean_tpot_us[g] = tpot;
                             S.B->rows.decode_tps[g] = tps;
                             S.B->rows.met_flags[g] = (uint8_t)((ttm ? 1 : 0) | (tpm ? 2 : 0) | ((ttm && tpm) ? 4 : 0));
-                            S.B->rows.deadline_misses[g] = miss;
+                            S.B->rows.deadline_misses[g] = sl.miss;
                             S.B->rows.t_last_token[g] = t;
                         }
                     }
                 }
                 unsigned rmask = __ballot_sync(FULLMASK, retire);
                 if (retire) {
-                    tps_buf[S.ntps + __popc(rmask & lanemask_lt(lane))] = tps;
-                    l_miss += miss;
-                    l_tpot += tpm;
-                    l_e2e += tpm && (flag & 2);
+                    tps_buf[ntps + __popc(rmask & lanemask_lt(lane))] = tps;
+                    S.l_miss += sl.miss;
+                    S.l_tpot += tpm;
+                    S.l_e2e += tpm && (sl.flag & 2);
                 }
-                S.ntps += __popc(rmask);
-                S.finished += __popc(rmask);
+                ntps += __popc(rmask);
+                finished += __popc(rmask);
                 if (FULL && S.T.buf) {
-                    unsigned bm = __ballot_sync(FULLMASK, inb);
-                    if (inb) S.T.put(tw0 + nmem + __popc(bm & lanemask_lt(lane)), pos);
-                    nmem += __popc(bm);
+                    if (inb) S.T.put(S.T.used + 5 + __popc(dc_mask & lanemask_lt(lane)), sl.pos);
+                    nmem = __popc(dc_mask);
                 }
-                // compact survivors (stable), clearing the in-batch bit
-                bool keep = v && !retire;
-                unsigned km = __ballot_sync(FULLMASK, keep);
-                __syncwarp();
-                if (keep) {
-                    int d = o + __popc(km & lanemask_lt(lane));
-                    a_pos[d] = pos; a_seq[d] = seq; a_idr[d] = idr; a_out[d] = outl; a_inp[d] = inp;
-                    a_miss[d] = miss; a_tf[d] = tf; a_flag[d] = flag & ~1;
-                    mx = seq > mx ? seq : mx;
-                }
-                o += __popc(km);
-                __syncwarp();
+                amask &= ~rmask;
+                amax = __reduce_max_sync(FULLMASK, ((amask >> lane) & 1u) ? sl.seq : 0);
+                // retiring reservations: one REDUX when every lane's value fits 26 bits
+                if (__all_sync(FULLMASK, kv_rel < (1LL << 26))) kv -= (int64_t)__reduce_add_sync(FULLMASK, (unsigned)kv_rel);
+                else kv -= wsum64(kv_rel);
+                s = __reduce_add_sync(FULLMASK, hsh);
+                an = __popc(amask);
+            } else {
+                SIM_SYNC_OUT();
+                on_decode_done_mem<FULL>(S, sl, t, s, nmem, lane);
+                SIM_SYNC_IN();
             }
-            S.an = o;
-            S.amax = __reduce_max_sync(FULLMASK, (int)mx);
-            // retiring reservations: one REDUX when every lane's sum fits 26 bits
-            if (__all_sync(FULLMASK, kv_rel < (1LL << 26))) S.kv -= (int64_t)__reduce_add_sync(FULLMASK, (unsigned)kv_rel);
-            else S.kv -= wsum64(kv_rel);
-            s = __reduce_add_sync(FULLMASK, s);
             if (use_lut) {
-                if (lane == 0) lut_update(L, S.dc_bsz, S.dc_max, S.dc_dur);
+                if (lane == 0) lut_update(L, dc_bsz, dc_max, dc_dur);
                 __syncwarp();
             }
-            S.dsteps++;
-            S.D = dstep(S.D, (uint64_t)t ^ 0x5A5A5A5A5A5A5A5AULL);
-            S.D = dstep(S.D, ((uint64_t)s << 32) | (uint32_t)S.dc_bsz);
-            S.D = dstep(S.D, (uint64_t)S.dc_dur);
+            dsteps++;
+            D = dstep(D, (uint64_t)t ^ 0x5A5A5A5A5A5A5A5AULL);
+            D = dstep(D, ((uint64_t)s << 32) | (uint32_t)dc_bsz);
+            D = dstep(D, (uint64_t)dc_dur);
             if (FULL && S.T.buf && lane == 0) {
-                S.T.put(S.T.used, SLOSIM_EV_DECODE_DONE); S.T.put(S.T.used + 1, t); S.T.put(S.T.used + 2, S.dc_dur);
-                S.T.put(S.T.used + 3, S.dc_bsz); S.T.put(S.T.used + 4, S.dc_max);
+                S.T.put(S.T.used, SLOSIM_EV_DECODE_DONE); S.T.put(S.T.used + 1, t); S.T.put(S.T.used + 2, dc_dur);
+                S.T.put(S.T.used + 3, dc_bsz); S.T.put(S.T.used + 4, dc_max);
             }
-            S.T.used += 5 + (FULL && S.T.buf ? nmem : 0);
-            S.dc_end = SLOSIM_INF64;
+            if (FULL) S.T.used += 5 + nmem;
+            dc_end = SLOSIM_INF64;
         }
 
-        if (S.pt > S.ph) on_admit<FULL>(S, t, lane);
-        if (S.pf_end == SLOSIM_INF64 && S.qt > S.qh) on_prefill_start<FULL>(S, t, lane);
+        // admission, then a new prefill step (out of line)
+        if (pt > ph || (pf_end == SLOSIM_INF64 && qt > qh)) {
+            SIM_SYNC_OUT();
+            if (S.pt > S.ph) on_admit<FULL>(S, sl, t, lane);
+            if (S.pf_end == SLOSIM_INF64 && S.qt > S.qh) on_prefill_start<FULL>(S, t, lane);
+            SIM_SYNC_IN();
+        }
 
         // ---- start a decode step (engine.py:377-392): the hot path
-        if (S.dc_end == SLOSIM_INF64 && S.an > 0) {
-            const int an = S.an;
-            S.v_dec += an;
-            S.max_a = an > S.max_a ? an : S.max_a;
+        if (dc_end == SLOSIM_INF64 && an > 0) {
+            v_dec += an;
+            max_a = an > max_a ? an : max_a;
             int bsz = an;
-            int64_t bmax = S.amax;
-            S.dc_prefix = an;
-            if (DP == SLOSIM_DECODE_KAIROS_SLACK) {
-                // select_decode_batch decode_sched.py:60-111
-                const int32_t* a_seq = w.i32(A_SEQ);
-                const int32_t* a_inp = w.i32(A_INP);
-                const int64_t* a_tf = w.i64(A_TFIRST);
-                double fallback = lut_lookup(L, an, S.amax);
-                int64_t sl = SLOSIM_INF64;
-#pragma unroll 1
-                for (int i = lane; i < an; i += 32) {
-                    int64_t ngen = (int64_t)a_seq[i] - a_inp[i];
-                    int64_t v = tpot_slo * (ngen + 1) - (t - a_tf[i]);
-                    sl = v < sl ? v : sl;
+            int64_t bmax = amax;
+            if (regmode) {
+                dc_mask = amask;
+                if (DP == SLOSIM_DECODE_KAIROS_SLACK) {
+                    dc_mask = 0;  // set below from the selection
+                    // select_decode_batch decode_sched.py:60-111
+                    double fallback = lut_lookup(L, an, amax);
+                    bool occ = (amask >> lane) & 1u;
+                    int64_t v = occ ? tpot_slo * ((int64_t)(sl.seq - sl.inp) + 1) - (t - sl.tf) : SLOSIM_INF64;
+                    double smin = xsub((double)wmin64_redux(v), fallback);
+                    uint32_t adm;
+                    int64_t ms;
+                    int b;
+                    if (L->full) {
+                        b = scan_slots(L, amask, an, sl, smin, adm, ms, lane);
+                    } else {
+                        // general LUT: memory-mode selection on a spilled copy
+                        SIM_SYNC_OUT();
+                        to_memory_mode(S, sl, lane);
+                        on_decode_start_mem<DP>(S, t, bsz, bmax, lane);
+                        // map the flag bits back to slots (slot order == compacted order)
+                        int d = __popc(amask & lanemask_lt(lane));
+                        bool f = ((amask >> lane) & 1u) && (S.w.i32(A_FLAG)[d] & 1);
+                        adm = __ballot_sync(FULLMASK, f);
+                        b = S.dc_prefix >= 0 ? 0 : bsz;
+                        ms = bmax;
+                        S.regmode = true;
+                        S.dc_prefix = -1;
+                        SIM_SYNC_IN();
+                    }
+                    if (b > 0) { bsz = b; bmax = ms; dc_mask = adm; }
+                    else { bsz = an; bmax = amax; dc_mask = amask; }
                 }
-                sl = wmin64(sl);
-                double smin = xsub((double)sl, fallback);
-                decode_order(an, a_seq, w.i32(A_IDR), w.i32(A_ORD), lane);
-                double tcur;
-                int64_t ms;
-                int b = decode_scan(L, an, w.i32(A_ORD), a_seq, w.i32(A_FLAG), smin, &tcur, &ms, nullptr, nullptr,
-                                    nullptr, nullptr, lane);
-                if (b > 0) { bsz = b; bmax = ms; S.dc_prefix = -1; }
+            } else {
+                SIM_SYNC_OUT();
+                on_decode_start_mem<DP>(S, t, bsz, bmax, lane);
+                SIM_SYNC_IN();
             }
-            S.b_dec += bsz;
+            b_dec += bsz;
             // _GroundTruth.decode_step_us engine.py:185-192
             const slosim_profile_t* P = S.P;
             double val = P->gt_frozen ? lut_lookup(cx.frozen_tab + pid, bsz, bmax)
@@ -1031,13 +1297,21 @@ __device__ __noinline__ void simulate(const Ctx& cx, int64_t ii, const WS& w, in
             double eps = P->noise_eps;
             if (eps > 0) val = xmul(val, pcg_uniform(rng, xsub(1.0, eps), xadd(1.0, eps)));
             int64_t d = rint_i64(val);
-            S.dc_dur = d < 1 ? 1 : d;
-            S.dc_bsz = bsz;
-            S.dc_max = bmax;
-            S.dc_end = t + S.dc_dur;
+            dc_dur = d < 1 ? 1 : d;
+            dc_bsz = bsz;
+            dc_max = bmax;
+            dc_end = t + dc_dur;
         }
     }
-    on_finalize<FULL>(S, l_tpot, l_e2e, l_miss, c0, lane);
+    SIM_SYNC_OUT();
+#undef SIM_SYNC_IN
+#undef SIM_SYNC_OUT
+    S.t_end = t_end;
+    S.dsteps = dsteps;
+    S.v_dec = v_dec;
+    S.b_dec = b_dec;
+    S.max_a = max_a;
+    on_finalize<FULL>(S, c0, lane);
 }
 
 #ifndef SLOSIM_MIN_BLOCKS

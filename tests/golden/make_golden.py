@@ -211,6 +211,9 @@ def main():
         make_event_golden(slosim)
         make_policy_golden(slosim)
         return
+    if os.environ.get("GOLDEN_ONLY") == "extra":
+        make_extra_golden(slosim)
+        return
 
     out = {"meta": {"reference": "slosim @ /root/reference/pkg/src", "numpy": __import__("numpy").__version__}}
     # --- config 1: 6 rates x 2 pairs on gen_longtail(LongTailSpec())
@@ -240,6 +243,79 @@ def main():
     print("wrote", path, os.path.getsize(path))
     make_event_golden(slosim)
     make_policy_golden(slosim)
+    make_extra_golden(slosim)
+
+
+def make_extra_golden(slosim):
+    """Engine cases for the less common device paths: file-backed sparse LUTs
+    (general lookup + frozen ground truth) and bursts with > 32 concurrently
+    active decodes (memory-mode active set, register/memory switching)."""
+    import tempfile
+
+    rng = random.Random(99)
+    cases = []
+    tmp = tempfile.mkdtemp()
+    for k in range(48):
+        sparse = k % 2 == 0
+        burst = rng.random() < 0.6
+        n = rng.randrange(40, 130) if burst else rng.randrange(20, 90)
+        wl = []
+        for i in range(n):
+            inp = rng.choice([rng.randrange(1, 900), rng.randrange(1, 5000), rng.randrange(20000, 70000)])
+            if burst:
+                inp = rng.randrange(1, 700)
+            arr = rng.randrange(0, 50_000) if burst else rng.randrange(0, 3_000_000)
+            wl.append(slosim.Request(id=f"x{i:03d}", arrival_time=arr, input_len=inp,
+                                     output_len=rng.choice([1, rng.randrange(2, 80), rng.randrange(50, 400)])
+                                     if not burst else rng.randrange(30, 300),
+                                     prefix_hit_len=rng.randrange(0, inp) if rng.random() < 0.1 else 0))
+        wl.sort(key=lambda r: r.arrival_time)
+        profile_json = None
+        if sparse:
+            bszs = sorted(rng.sample(range(1, 80), rng.randrange(2, 7)))
+            seqs = sorted(rng.sample(range(500, 150_000), rng.randrange(2, 9)))
+            entries, counts = [], []
+            for b in bszs:
+                er, cr = [], []
+                for sq in seqs:
+                    if rng.random() < 0.6:
+                        er.append(float(rng.randrange(3_000, 60_000)) + rng.choice([0.0, 0.25, 0.5]))
+                        cr.append(rng.randrange(1, 50))
+                    else:
+                        er.append(0.0)
+                        cr.append(0)
+                entries.append(er)
+                counts.append(cr)
+            if not any(c for row in counts for c in row):
+                counts[0][0] = 3
+                entries[0][0] = 9_000.0
+            profile_json = {"bsz_buckets": bszs, "seq_buckets": seqs, "entries_us": entries, "counts": counts,
+                            "prefill_anchor": {"tokens": rng.choice([10_000, 131072]),
+                                               "duration_us": rng.choice([1_000_000, 8_800_000])}}
+            path = os.path.join(tmp, f"p{k}.json")
+            with open(path, "w") as f:
+                json.dump(profile_json, f)
+            prof = slosim.CostProfile(profile_path=path, decode_noise_eps=rng.choice([0.0, 0.2]))
+        else:
+            prof = slosim.CostProfile(decode_noise_eps=rng.choice([0.0, 0.2]))
+        pp = ["fcfs", "sjf", "kairos-urgency"][k % 3]
+        dp = ["continuous", "kairos-slack"][(k // 3) % 2]
+        cfg = slosim.ClusterConfig(prefill_policy=pp, decode_policy=dp, profile=prof, seed=rng.randrange(100),
+                                   kv_capacity_tokens=rng.choice([2_000_000, 400_000, 150_000]),
+                                   chunk_budget=rng.choice([8192, 2048]),
+                                   slo=slosim.SLOConfig(tpot_slo_us=rng.choice([50_000, 150_000, 400_000])))
+        try:
+            s = run_reference(slosim, cfg, wl)
+        except slosim.ConfigurationError:
+            continue
+        cj = cfg_to_json(cfg)
+        cj["profile"]["profile_json"] = profile_json
+        cases.append({"workload": wl_to_json(wl), "config": cj, "summary": s})
+    path = os.path.join(HERE, "extra_golden.json.gz")
+    with gzip.open(path, "wt", encoding="utf-8") as f:
+        json.dump(cases, f, sort_keys=True)
+    print("wrote", path, len(cases), "max_active", max(c["summary"].get("max_active", 0) for c in cases),
+          os.path.getsize(path))
 
 
 def make_event_golden(slosim):

@@ -23,8 +23,35 @@ def load_golden(name="engine_golden.json.gz"):
         return json.load(f)
 
 
+_PROFILE_DIR = None
+
+
+def _profile_file(profile_json) -> str:
+    """Materialise a file-backed profile (costmodel.py:312-334 format) for profile_path."""
+    global _PROFILE_DIR
+    import hashlib
+    import tempfile
+
+    if _PROFILE_DIR is None:
+        _PROFILE_DIR = tempfile.mkdtemp(prefix="slosim_profiles_")
+    text = json.dumps(profile_json, sort_keys=True)
+    path = os.path.join(_PROFILE_DIR, hashlib.sha1(text.encode()).hexdigest() + ".json")
+    if not os.path.exists(path):
+        with open(path, "w") as f:
+            f.write(text)
+    return path
+
+
 def cfg_from_json(c) -> ClusterConfig:
     p = c["profile"]
+    if p.get("profile_json"):
+        prof = CostProfile(profile_path=_profile_file(p["profile_json"]), decode_noise_eps=p["decode_noise_eps"])
+        return ClusterConfig(
+            chunk_budget=c["chunk_budget"], kv_capacity_tokens=c["kv_capacity_tokens"],
+            transfer_base_us=c["transfer_base_us"], transfer_per_token_us=c["transfer_per_token_us"],
+            prefill_policy=c["prefill_policy"], decode_policy=c["decode_policy"],
+            slo=SLOConfig(c["ttft_slo_us"], c["tpot_slo_us"]), profile=prof, seed=c["seed"],
+        )
     prof = CostProfile(
         decode_anchors=[tuple(a) for a in p["decode_anchors"]], batch_growth=p["batch_growth"],
         prior_weight=p["prior_weight"], bsz_buckets=p["bsz_buckets"], seq_buckets=p["seq_buckets"],

@@ -57,6 +57,28 @@ def test_random_cases_match_reference_golden(golden, lib):
     assert not bad, f"{len(bad)} cases differ: {dict(list(bad.items())[:5])}"
 
 
+def test_sparse_profiles_and_wide_active_sets_match_reference_golden(lib):
+    """File-backed sparse LUTs (general lookup/scan paths, frozen ground truth) and bursts with
+    up to 123 concurrent decodes (memory-mode active set and register/memory switching)."""
+    from paper_2605_02329_b200 import _abi
+    from paper_2605_02329_b200.batch import run_batch
+
+    cases = load_golden("extra_golden.json.gz")
+    packed, _ = pack_cases(cases, flags=_abi.F_ROWS)
+    got = run_batch(packed)
+    bad = {}
+    for i, c in enumerate(cases):
+        m = summary_mismatches(got[i], c["summary"]) + row_mismatches(packed, i, c["summary"]["rows"])[:3]
+        if m:
+            bad[i] = m
+    assert not bad, f"{len(bad)} cases differ: {dict(list(bad.items())[:5])}"
+    # the same cases through the throughput specialisation (no rows, no trace)
+    packed2, _ = pack_cases(cases, flags=0)
+    got2 = run_batch(packed2)
+    for i, c in enumerate(cases):
+        assert summary_mismatches(got2[i], c["summary"]) == [], i
+
+
 def test_host_buffer_entry_point_matches(golden, lib):
     """slosim_run_batch_host (host buffers, copies inside) gives the same rows as the device path."""
     from paper_2605_02329_b200 import _abi

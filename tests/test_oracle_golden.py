@@ -75,6 +75,16 @@ def test_oracle_random_cases_match_reference(golden):
             assert row_mismatches(packed, i, c["summary"]["rows"]) == [], i
 
 
+def test_oracle_sparse_profiles_and_bursts_match_reference():
+    """File-backed sparse LUTs (general lookup, frozen ground truth) and > 32 active decodes."""
+    cases = load_golden("extra_golden.json.gz")
+    packed, _ = pack_cases(cases, synth=oracle.synth)
+    oracle.run_batch(packed, threads=4)
+    for i, c in enumerate(cases):
+        assert summary_mismatches(packed.summaries[i], c["summary"]) == [], i
+        assert row_mismatches(packed, i, c["summary"]["rows"]) == [], i
+
+
 def test_oracle_event_logs_match_reference():
     """Full event logs, token timestamps, final LUT and estimator vs Simulation(collect_events=True)."""
     G = load_golden("events_golden.json.gz")
