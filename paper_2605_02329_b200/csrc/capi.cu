@@ -146,6 +146,26 @@ struct Owned {
 };
 }  // namespace
 
+// Default processing order of the persistent work queue (same rule as
+// batch.schedule_order): group by decode policy (slack-guided first) so each
+// SM runs one specialised engine loop at a time, longest-first inside a group
+// (cost = n_requests x arrival stretch factor).
+static void default_order(const slosim_batch_t* hb, std::vector<int64_t>& order) {
+    size_t n = (size_t)hb->n_instances;
+    order.resize(n);
+    std::vector<double> cost(n);
+    for (size_t i = 0; i < n; i++) {
+        order[i] = (int64_t)i;
+        const slosim_instance_t& x = hb->instances[i];
+        cost[i] = (double)x.n_requests * (x.rescale_factor > 0 ? x.rescale_factor : 1.0);
+    }
+    std::stable_sort(order.begin(), order.end(), [&](int64_t a, int64_t b) {
+        int da = hb->instances[a].decode_policy, db = hb->instances[b].decode_policy;
+        if (da != db) return da > db;
+        return cost[a] > cost[b];
+    });
+}
+
 extern "C" int slosim_run_batch_host(const slosim_batch_t* hb, float* elapsed_ms) {
     if (!hb) return SLOSIM_EINVAL;
     Owned o;
@@ -180,6 +200,10 @@ extern "C" int slosim_run_batch_host(const slosim_batch_t* hb, float* elapsed_ms
     bool lut = (hb->flags & SLOSIM_F_EXPORT_LUT) && hb->lut_out_sums;
     CK(alloc(&d.lut_out_sums, lut ? ni * FR : 0, o.v));
     CK(alloc(&d.lut_out_counts, lut ? ni * FR : 0, o.v));
+    std::vector<int64_t> order;
+    if (hb->order) order.assign(hb->order, hb->order + ni);
+    else default_order(hb, order);
+    CK(up((int64_t**)&d.order, order.data(), ni, o.v));
     cudaEvent_t e0, e1;
     CK(cudaEventCreate(&e0));
     CK(cudaEventCreate(&e1));
