@@ -1029,7 +1029,7 @@ __device__ __forceinline__ int scan_slots(const LutMem* L, uint32_t amask, int a
         double xprev = __shfl_sync(FULLMASK, x, pred);
         double tprev = rank == s ? tcur : xprev;
         int64_t bprev = bx - 1;
-        bool okx = valid && x <= smin && (bprev == 0 || xdiv((double)(bprev + 1), x) > xdiv((double)bprev, tprev));
+        bool okx = valid && x <= smin && (bprev == 0 || quot_gt((double)(bprev + 1), x, (double)bprev, tprev));
         int f = __reduce_min_sync(FULLMASK, (valid && !okx) ? rank : an);
         adm |= __ballot_sync(FULLMASK, valid && rank < f);
         if (f > s) {
@@ -1041,10 +1041,9 @@ __device__ __forceinline__ int scan_slots(const LutMem* L, uint32_t amask, int a
             continue;
         }
         RowSel rs = lut_rows(L, b + 1);
-        double thr = b ? xdiv((double)b, tcur) : 0.0;
         bool vy = occ && rank > s;
         double y = vy ? lut_eval(L, rs, cs) : 0.0;
-        bool oky = vy && y <= smin && (b == 0 || xdiv((double)(b + 1), y) > thr);
+        bool oky = vy && y <= smin && (b == 0 || quot_gt((double)(b + 1), y, (double)b, tcur));
         int g = __reduce_min_sync(FULLMASK, oky ? rank : an);
         if (g >= an) break;
         int lg = __ffs((int)__ballot_sync(FULLMASK, occ && rank == g)) - 1;
@@ -1223,7 +1222,7 @@ __device__ __noinline__ void simulate(const Ctx& cx, int64_t ii, const WS& w, in
                 SIM_SYNC_IN();
             }
             if (use_lut) {
-                if (lane == 0) lut_update(L, dc_bsz, dc_max, dc_dur);
+                lut_update_warp(L, dc_bsz, dc_max, dc_dur, lane);
                 __syncwarp();
             }
             dsteps++;

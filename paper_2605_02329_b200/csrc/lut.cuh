@@ -263,6 +263,34 @@ __device__ void lut_update(LutMem* L, int64_t bsz, int64_t max_seq, int64_t obs)
     if (prev) lut_fix_slope(L, i, 63 - __clzll((long long)prev));
 }
 
+// Warp form of lut_update: on a fully populated grid lanes 0-2 compute the new
+// cell mean and the np.interp slopes into and out of the cell concurrently
+// (neighbouring columns are the populated neighbours); otherwise lane 0 runs
+// the general update.
+__device__ __forceinline__ void lut_update_warp(LutMem* L, int64_t bsz, int64_t max_seq, int64_t obs, int lane) {
+    if (!L->full) {
+        if (lane == 0) lut_update(L, bsz, max_seq, obs);
+        return;
+    }
+    int i = lut_bidx(L, bsz), j = lut_sidx(L, max_seq);
+    const int nb = L->nb, ns = L->ns;
+    i = i < nb - 1 ? i : nb - 1;
+    j = j < ns - 1 ? j : ns - 1;
+    const int c = i * ns + j;
+    double sum = xadd(L->sum[c], (double)obs);
+    int32_t cnt = L->cnt[c] + 1;
+    double mean = xdiv(sum, (double)cnt);
+    // lane 0: the cell; lane 1: slope (j -> j+1); lane 2: slope (j-1 -> j)
+    if (lane == 0) { L->sum[c] = sum; L->cnt[c] = cnt; L->mean[c] = mean; }
+    bool right = lane == 1 && j + 1 < ns, left = lane == 2 && j > 0;
+    if (right || left) {
+        int a = right ? j : j - 1;
+        double ma = right ? mean : L->mean[c - 1];
+        double mb = right ? L->mean[c + 1] : mean;
+        L->slope[i * ns + a] = xdiv(xsub(mb, ma), xsub((double)L->sb[a + 1], (double)L->sb[a]));
+    }
+}
+
 // _interp_clamped costmodel.py:32-47 (Python form y0 + (y1-y0)*(x-x0)/(x1-x0)).
 __device__ __forceinline__ double interp_clamped(int n, const int64_t* px, const double* py, int64_t x) {
     if (x <= px[0]) return py[0];

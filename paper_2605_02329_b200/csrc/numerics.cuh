@@ -15,6 +15,18 @@ __device__ __forceinline__ double xsub(double a, double b) { return __dsub_rn(a,
 __device__ __forceinline__ double xmul(double a, double b) { return __dmul_rn(a, b); }
 __device__ __forceinline__ double xdiv(double a, double b) { return __ddiv_rn(a, b); }
 
+// RN(a/x) > RN(b/y) for a > b >= 1 small integers and x, y > 0 finite (the
+// throughput test of decode_sched.py:87-89).  The products a*y and b*x carry
+// at most 2^-53 relative error each; when they differ by more than 2^-50
+// relative, the exact quotients differ by more than the two roundings can
+// close, so the product comparison decides; otherwise divide exactly.
+__device__ __forceinline__ bool quot_gt(double a, double x, double b, double y) {
+    double p = __dmul_rn(a, y), q = __dmul_rn(b, x);
+    if (p > __dmul_rn(q, 1.0 + 0x1p-50)) return true;
+    if (p < __dmul_rn(q, 1.0 - 0x1p-50)) return false;
+    return __ddiv_rn(a, x) > __ddiv_rn(b, y);
+}
+
 // Python round(x) for floats: half-to-even (engine.py:183,192; costmodel.py:303).
 __device__ __forceinline__ int64_t rint_i64(double x) { return __double2ll_rn(x); }
 
