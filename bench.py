@@ -80,12 +80,13 @@ def load_peaks():
         return 6650.0, "fallback"
 
 
-def profile_traffic():
-    """dram bytes per launch of the dominant kernel from the committed ncu summary, if any."""
+def profile_traffic(instances_per_launch):
+    """DRAM bytes per launch of the dominant kernel from the committed `ncu --set full` capture
+    (profiles/ncu_summary.json), scaled per instance to this launch size; None if absent."""
     try:
         with open(os.path.join(ROOT, "profiles", "ncu_summary.json")) as f:
             d = json.load(f)
-        return d.get("dram_bytes_per_launch"), d.get("alg_bytes_per_launch")
+        return d["dram_bytes_per_instance"] * instances_per_launch, d.get("capture")
     except Exception:
         return None, None
 
@@ -215,9 +216,14 @@ def main():
     from paper_2605_02329_b200.batch import DeviceBatch
 
     world, rank, local = dist_env()
-    torch.cuda.set_device(local)
+    dev = local % max(torch.cuda.device_count(), 1)
+    torch.cuda.set_device(dev)
+    backend = os.environ.get("SLOSIM_DIST_BACKEND", "nccl")  # gloo: N ranks sharing one GPU (testing)
     if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", dev))
+        else:
+            dist.init_process_group(backend)
     L = _abi.lib()
 
     # full instance grid resident in HBM (instances + traces), summaries per instance
@@ -243,7 +249,7 @@ def main():
     torch.cuda.synchronize()
     timed = D.slices_for_rank(n_slices, world, rank, args.steps, args.warmup)
     ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in timed]
-    clk = ClockSampler(local)
+    clk = ClockSampler(dev)
     time.sleep(0.3)
     if world > 1:
         dist.barrier()
@@ -272,7 +278,7 @@ def main():
     clocks = clk.stop()
     elapsed_ms = t_start.elapsed_time(t_end)
     step_ms = [e0.elapsed_time(e1) for e0, e1 in ev]
-    tmax = torch.tensor([elapsed_ms], dtype=torch.float64, device="cuda")
+    tmax = torch.tensor([elapsed_ms], dtype=torch.float64, device="cuda" if backend == "nccl" else "cpu")
     if world > 1:
         dist.all_reduce(tmax, op=dist.ReduceOp.MAX)
     elapsed_ms = float(tmax.item())
@@ -290,7 +296,7 @@ def main():
     abytes = alg_bytes(summ) / len(timed)
     mean_ms = float(np.mean(step_ms))
     achieved = abytes / (mean_ms / 1e3) / 1e9
-    traffic, _ = profile_traffic()
+    traffic, traffic_src = profile_traffic(slice_n)
 
     # e2e through the C-ABI with host buffers (pinned), copies inside the timed region
     e2e = None
@@ -312,6 +318,7 @@ def main():
             "e2e": e2e,
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "peak_kind": peak_kind, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": traffic,
+                         "traffic_source": f"ncu dram__bytes_read+write per instance x {slice_n} ({traffic_src})",
                          "alg_bytes_per_launch": abytes, "mean_launch_ms": mean_ms},
             "cpu_baseline": cpu,
             "parity": parity,
@@ -351,7 +358,8 @@ def measure_e2e(args, sw, timed, slice_n, world):
     T = sum(times)
     import torch.distributed as dist
 
-    t = torch.tensor([T], dtype=torch.float64, device="cuda")
+    on_gpu = not (dist.is_available() and dist.is_initialized()) or dist.get_backend() == "nccl"
+    t = torch.tensor([T], dtype=torch.float64, device="cuda" if on_gpu else "cpu")
     if dist.is_available() and dist.is_initialized():
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
     return {"value": reqs * world / float(t.item()), "unit": "simulated requests/s", "h2d_bytes_per_step": h2d,

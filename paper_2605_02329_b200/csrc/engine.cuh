@@ -1154,7 +1154,7 @@ __device__ __noinline__ void simulate(const Ctx& cx, int64_t ii, const WS& w, in
         t_end = t;
 
         // rare events (a few per request) run out of line, in the reference's order
-        if (next_arr == t || tr_min == t || pf_end == t) {
+        if (__builtin_expect(next_arr == t || tr_min == t || pf_end == t, 0)) {
             SIM_SYNC_OUT();
             if (S.next_arr == t) on_arrivals<FULL>(S, t, lane);
             if (S.tr_min == t) on_transfers<FULL>(S, t, lane);
@@ -1166,7 +1166,7 @@ __device__ __noinline__ void simulate(const Ctx& cx, int64_t ii, const WS& w, in
         if (dc_end == t) {
             uint32_t s = 0;
             int nmem = 0;
-            if (regmode) {
+            if (__builtin_expect(regmode, 1)) {
                 bool inb = (dc_mask >> lane) & 1u;
                 bool retire = false, tpm = false;
                 double tps = 0.0;
@@ -1177,7 +1177,7 @@ __device__ __noinline__ void simulate(const Ctx& cx, int64_t ii, const WS& w, in
                     int64_t ngen = sl.seq - sl.inp;
                     hsh = member_hash((uint32_t)sl.pos);
                     if (t > sl.tf + ngen * tpot_slo) sl.miss++;  // deadline_misses metrics.py:57-69
-                    if (ngen == sl.out - 1) {
+                    if (__builtin_expect(ngen == sl.out - 1, 0)) {
                         // request_metrics metrics.py:72-84 at retirement
                         retire = true;
                         int64_t span = t - sl.tf;
@@ -1197,7 +1197,7 @@ __device__ __noinline__ void simulate(const Ctx& cx, int64_t ii, const WS& w, in
                     }
                 }
                 unsigned rmask = __ballot_sync(FULLMASK, retire);
-                if (retire) {
+                if (__builtin_expect(retire, 0)) {
                     tps_buf[ntps + __popc(rmask & lanemask_lt(lane))] = tps;
                     S.l_miss += sl.miss;
                     S.l_tpot += tpm;
@@ -1238,7 +1238,7 @@ __device__ __noinline__ void simulate(const Ctx& cx, int64_t ii, const WS& w, in
         }
 
         // admission, then a new prefill step (out of line)
-        if (pt > ph || (pf_end == SLOSIM_INF64 && qt > qh)) {
+        if (__builtin_expect(pt > ph || (pf_end == SLOSIM_INF64 && qt > qh), 0)) {
             SIM_SYNC_OUT();
             if (S.pt > S.ph) on_admit<FULL>(S, sl, t, lane);
             if (S.pf_end == SLOSIM_INF64 && S.qt > S.qh) on_prefill_start<FULL>(S, t, lane);
@@ -1251,7 +1251,7 @@ __device__ __noinline__ void simulate(const Ctx& cx, int64_t ii, const WS& w, in
             max_a = an > max_a ? an : max_a;
             int bsz = an;
             int64_t bmax = amax;
-            if (regmode) {
+            if (__builtin_expect(regmode, 1)) {
                 dc_mask = amask;
                 if (DP == SLOSIM_DECODE_KAIROS_SLACK) {
                     dc_mask = 0;  // set below from the selection
@@ -1263,7 +1263,7 @@ __device__ __noinline__ void simulate(const Ctx& cx, int64_t ii, const WS& w, in
                     uint32_t adm;
                     int64_t ms;
                     int b;
-                    if (L->full) {
+                    if (__builtin_expect(L->full, 1)) {
                         b = scan_slots(L, amask, an, sl, smin, adm, ms, lane);
                     } else {
                         // general LUT: memory-mode selection on a spilled copy

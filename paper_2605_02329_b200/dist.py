@@ -53,10 +53,13 @@ def exchange(summary_bytes, hist, group=None):
     if not (dist.is_available() and dist.is_initialized()) or dist.get_world_size(group) == 1:
         return summary_bytes, hist
     world = dist.get_world_size(group)
+    dev = hist.device
+    if dist.get_backend(group) != "nccl" and dev.type == "cuda":  # gloo: exchange through host copies
+        summary_bytes, hist = summary_bytes.cpu(), hist.cpu()
     dist.all_reduce(hist, op=dist.ReduceOp.SUM, group=group)
     out = torch.empty(world * summary_bytes.numel(), dtype=summary_bytes.dtype, device=summary_bytes.device)
     dist.all_gather_into_tensor(out, summary_bytes, group=group)
-    return out, hist
+    return out.to(dev), hist.to(dev)
 
 
 def summaries_from_bytes(buf) -> np.ndarray:
