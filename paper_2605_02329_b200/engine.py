@@ -82,6 +82,26 @@ def decode_trace(words: np.ndarray):
     return recs
 
 
+def check_config(config: ClusterConfig, workload: list):
+    """The refusals of Simulation.__init__ (engine.py:218-232), in the same order.
+
+    Returns the initial (DecodeStepLUT, PrefillThroughputEstimator); raises ConfigurationError.
+    """
+    lut = config.profile.build_lut()
+    if lut.is_empty:
+        raise ConfigurationError("decode LUT has no populated entries")
+    est = config.profile.build_estimator()
+    if config.profile.profile_path is None and not any(a[0] == 1 for a in config.profile.decode_anchors):
+        raise ConfigurationError("decode anchors need at least one bsz=1 entry")
+    worst = max((r.input_len + r.output_len for r in workload), default=0)
+    if worst > config.kv_capacity_tokens:
+        raise ConfigurationError(
+            f"kv_capacity_tokens={config.kv_capacity_tokens} cannot hold the "
+            f"largest request reservation ({worst} tokens)"
+        )
+    return lut, est
+
+
 class Simulation:
     """One deterministic run of a workload against a cluster configuration (engine.py:195-413)."""
 
@@ -89,18 +109,7 @@ class Simulation:
         self.config = config
         _validate(workload)
         self.requests = copy.deepcopy(workload)
-        self.lut = config.profile.build_lut()
-        if self.lut.is_empty:
-            raise ConfigurationError("decode LUT has no populated entries")
-        self.estimator = config.profile.build_estimator()
-        if config.profile.profile_path is None and not any(a[0] == 1 for a in config.profile.decode_anchors):
-            raise ConfigurationError("decode anchors need at least one bsz=1 entry")
-        worst = max((r.input_len + r.output_len for r in self.requests), default=0)
-        if worst > config.kv_capacity_tokens:
-            raise ConfigurationError(
-                f"kv_capacity_tokens={config.kv_capacity_tokens} cannot hold the "
-                f"largest request reservation ({worst} tokens)"
-            )
+        self.lut, self.estimator = check_config(config, self.requests)
         self.events = [] if collect_events else None
         self._ran = False
 
