@@ -489,6 +489,7 @@ struct Sim {
     int64_t misses, worst_wait, psteps, dsteps, v_dec, b_dec, v_pre, t_end, l_miss;
     uint64_t D;
     TraceW T;
+    Pcg64 rng;  // decode noise (engine.py:191), drawn only when noise_eps > 0
 };
 
 // One active decode request held in a lane's registers (engine.py:374 _active).
@@ -889,7 +890,6 @@ __device__ __noinline__ void on_decode_done_mem(Sim& S, Slot& sl, int64_t t, uin
     int32_t* a_miss = w.i32(A_MISS);
     int32_t* a_flag = w.i32(A_FLAG);
     int64_t* a_tf = w.i64(A_TFIRST);
-    double* tps_buf = w.f64(TPS);
     uint32_t s = 0;
     int64_t kv_rel = 0, mx = 0;
     int o = 0;
@@ -934,7 +934,7 @@ __device__ __noinline__ void on_decode_done_mem(Sim& S, Slot& sl, int64_t t, uin
         }
         unsigned rmask = __ballot_sync(FULLMASK, retire);
         if (retire) {
-            tps_buf[S.ntps + __popc(rmask & lanemask_lt(lane))] = tps;
+            S.w.f64(TPS)[S.ntps + __popc(rmask & lanemask_lt(lane))] = tps;
             S.l_miss += miss;
             S.l_tpot += tpm;
             S.l_e2e += tpm && (flag & 2);
@@ -1056,6 +1056,48 @@ __device__ __forceinline__ int scan_slots(const LutMem* L, uint32_t amask, int a
     return b;
 }
 
+// Ground-truth decode step for frozen (file-backed) profiles and/or noise
+// (engine.py:185-192): out of the hot loop, which then carries neither the
+// general LUT lookup nor the PCG64 state.
+__device__ __noinline__ double gt_decode_cold(Sim& S, const LutMem* frozen, int64_t bsz, int64_t bmax) {
+    const slosim_profile_t* P = S.P;
+    double val = P->gt_frozen ? lut_lookup(frozen, bsz, bmax)
+                              : decode_formula(P->n_base, P->base_x, P->base_y, P->gamma, bsz, bmax);
+    double eps = P->noise_eps;
+    if (eps > 0) val = xmul(val, pcg_uniform(S.rng, xsub(1.0, eps), xadd(1.0, eps)));
+    return val;
+}
+
+// request_metrics (metrics.py:72-84) for the requests retiring at t, one per
+// lane with `retire` set; appends their decode tps at tps_buf[ntps..] in lane
+// order and returns the warp's released KV reservation.
+template <bool FULL>
+__device__ __noinline__ int64_t on_retire(Sim& S, const Slot sl, int64_t t, bool retire, int ntps, int lane) {
+    unsigned rmask = __ballot_sync(FULLMASK, retire);
+    int64_t kv_rel = 0;
+    if (retire) {
+        int64_t span = t - sl.tf;
+        double tpot = idiv(span, (int64_t)(sl.out - 1));
+        bool tpm = tpot <= (double)S.tpot_slo;
+        double tps = xdiv((double)(sl.out - 1), xdiv((double)span, 1e6));
+        kv_rel = (int64_t)sl.inp + sl.out;
+        if (FULL && S.rows) {
+            bool ttm = (sl.flag & 2) != 0;
+            int64_t g = S.row0 + sl.pos;
+            S.B->rows.mean_tpot_us[g] = tpot;
+            S.B->rows.decode_tps[g] = tps;
+            S.B->rows.met_flags[g] = (uint8_t)((ttm ? 1 : 0) | (tpm ? 2 : 0) | ((ttm && tpm) ? 4 : 0));
+            S.B->rows.deadline_misses[g] = sl.miss;
+            S.B->rows.t_last_token[g] = t;
+        }
+        S.w.f64(TPS)[ntps + __popc(rmask & lanemask_lt(lane))] = tps;
+        S.l_miss += sl.miss;
+        S.l_tpot += tpm;
+        S.l_e2e += tpm && (sl.flag & 2);
+    }
+    return wsum64(kv_rel);
+}
+
 // DP: decode policy (compile-time), FULL: event trace / per-request rows / LUT
 // export compiled in.  The throughput path runs simulate<DP, false>, whose hot
 // loop carries no tracing or row-output code.
@@ -1104,7 +1146,7 @@ __device__ __noinline__ void simulate(const Ctx& cx, int64_t ii, const WS& w, in
     if (use_lut) lut_copy(L, ST, lane);
     S.est_tok = S.P->est_tokens;
     S.est_busy = S.P->est_busy_us;
-    Pcg64 rng{I->rng_state_hi, I->rng_state_lo, I->rng_inc_hi, I->rng_inc_lo};
+    S.rng = Pcg64{I->rng_state_hi, I->rng_state_lo, I->rng_inc_hi, I->rng_inc_lo};
     S.T = TraceW{nullptr, 0, 0};
     if (FULL && S.B->trace_buf && I->trace_buf_offset >= 0) {
         S.T.buf = S.B->trace_buf + I->trace_buf_offset;
@@ -1123,7 +1165,6 @@ __device__ __noinline__ void simulate(const Ctx& cx, int64_t ii, const WS& w, in
     S.D = 0;
     Slot sl{0, 0, 0, 0, 0, 0, 0, 0};
     const int64_t tpot_slo = S.tpot_slo;
-    double* tps_buf = w.f64(TPS);
 
     // hot state in registers; synced with S around the (rare) out-of-line calls
     int64_t next_arr, pf_end, dc_end, tr_min, dc_dur, dc_bsz, dc_max, amax, kv, t_end = 0;
@@ -1168,52 +1209,27 @@ __device__ __noinline__ void simulate(const Ctx& cx, int64_t ii, const WS& w, in
             int nmem = 0;
             if (__builtin_expect(regmode, 1)) {
                 bool inb = (dc_mask >> lane) & 1u;
-                bool retire = false, tpm = false;
-                double tps = 0.0;
-                int64_t kv_rel = 0;
+                bool retire = false;
                 uint32_t hsh = 0;
                 if (inb) {
                     sl.seq += 1;
                     int64_t ngen = sl.seq - sl.inp;
                     hsh = member_hash((uint32_t)sl.pos);
                     if (t > sl.tf + ngen * tpot_slo) sl.miss++;  // deadline_misses metrics.py:57-69
-                    if (__builtin_expect(ngen == sl.out - 1, 0)) {
-                        // request_metrics metrics.py:72-84 at retirement
-                        retire = true;
-                        int64_t span = t - sl.tf;
-                        double tpot = idiv(span, (int64_t)(sl.out - 1));
-                        tpm = tpot <= (double)tpot_slo;
-                        tps = xdiv((double)(sl.out - 1), xdiv((double)span, 1e6));
-                        kv_rel = (int64_t)sl.inp + sl.out;
-                        if (FULL && S.rows) {
-                            bool ttm = (sl.flag & 2) != 0;
-                            int64_t g = S.row0 + sl.pos;
-                            S.B->rows.mean_tpot_us[g] = tpot;
-                            S.B->rows.decode_tps[g] = tps;
-                            S.B->rows.met_flags[g] = (uint8_t)((ttm ? 1 : 0) | (tpm ? 2 : 0) | ((ttm && tpm) ? 4 : 0));
-                            S.B->rows.deadline_misses[g] = sl.miss;
-                            S.B->rows.t_last_token[g] = t;
-                        }
-                    }
+                    retire = ngen == sl.out - 1;
                 }
                 unsigned rmask = __ballot_sync(FULLMASK, retire);
-                if (__builtin_expect(retire, 0)) {
-                    tps_buf[ntps + __popc(rmask & lanemask_lt(lane))] = tps;
-                    S.l_miss += sl.miss;
-                    S.l_tpot += tpm;
-                    S.l_e2e += tpm && (sl.flag & 2);
+                if (__builtin_expect(rmask != 0, 0)) {
+                    kv -= on_retire<FULL>(S, sl, t, retire, ntps, lane);
+                    ntps += __popc(rmask);
+                    finished += __popc(rmask);
+                    amask &= ~rmask;
                 }
-                ntps += __popc(rmask);
-                finished += __popc(rmask);
                 if (FULL && S.T.buf) {
                     if (inb) S.T.put(S.T.used + 5 + __popc(dc_mask & lanemask_lt(lane)), sl.pos);
                     nmem = __popc(dc_mask);
                 }
-                amask &= ~rmask;
                 amax = __reduce_max_sync(FULLMASK, ((amask >> lane) & 1u) ? sl.seq : 0);
-                // retiring reservations: one REDUX when every lane's value fits 26 bits
-                if (__all_sync(FULLMASK, kv_rel < (1LL << 26))) kv -= (int64_t)__reduce_add_sync(FULLMASK, (unsigned)kv_rel);
-                else kv -= wsum64(kv_rel);
                 s = __reduce_add_sync(FULLMASK, hsh);
                 an = __popc(amask);
             } else {
@@ -1289,12 +1305,13 @@ __device__ __noinline__ void simulate(const Ctx& cx, int64_t ii, const WS& w, in
                 SIM_SYNC_IN();
             }
             b_dec += bsz;
-            // _GroundTruth.decode_step_us engine.py:185-192
+            // _GroundTruth.decode_step_us engine.py:185-192 (frozen profiles and noise out of line)
             const slosim_profile_t* P = S.P;
-            double val = P->gt_frozen ? lut_lookup(cx.frozen_tab + pid, bsz, bmax)
-                                      : decode_formula(P->n_base, P->base_x, P->base_y, P->gamma, bsz, bmax);
-            double eps = P->noise_eps;
-            if (eps > 0) val = xmul(val, pcg_uniform(rng, xsub(1.0, eps), xadd(1.0, eps)));
+            double val;
+            if (__builtin_expect(P->gt_frozen == 0 && P->noise_eps <= 0.0, 1))
+                val = decode_formula(P->n_base, P->base_x, P->base_y, P->gamma, bsz, bmax);
+            else
+                val = gt_decode_cold(S, cx.frozen_tab + pid, bsz, bmax);
             int64_t d = rint_i64(val);
             dc_dur = d < 1 ? 1 : d;
             dc_bsz = bsz;

@@ -241,7 +241,7 @@ __device__ __forceinline__ double lut_lookup(const LutMem* L, int64_t bsz, int64
 }
 
 // DecodeStepLUT.update costmodel.py:118-128 (single thread; caller syncs the warp).
-__device__ void lut_update(LutMem* L, int64_t bsz, int64_t max_seq, int64_t obs) {
+__device__ __noinline__ void lut_update(LutMem* L, int64_t bsz, int64_t max_seq, int64_t obs) {
     // _bucket_index: smallest bucket >= key, clamped to the last (table lookups)
     int i = lut_bidx(L, bsz), j = lut_sidx(L, max_seq);
     i = i < L->nb - 1 ? i : L->nb - 1;
