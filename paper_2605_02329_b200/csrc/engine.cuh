@@ -1003,11 +1003,14 @@ __device__ __noinline__ void on_decode_start_mem(Sim& S, int64_t t, int& bsz, in
 // failing rank ends the admitted run.  If rank s itself fails, Y tests the rest
 // with the unchanged (|B|, t_cur) and admits the lowest admissible rank.
 // Returns |B| (0 = fallback) and the admitted slot mask.
-__device__ __forceinline__ int scan_slots(const LutMem* L, uint32_t amask, int an, const Slot& sl, double smin,
+// The fallback cost lookup(|A|, max_seq) (decode_sched.py:75) is the first
+// round's evaluation of the last-ranked slot (|B| = an at its seq_len = max_seq),
+// so s_min = min(v) - that value is formed after the first evaluation.
+__device__ __forceinline__ int scan_slots(const LutMem* L, uint32_t amask, int an, const Slot& sl, int64_t vmin,
                                           uint32_t& adm, int64_t& mseq, int lane) {
     bool occ = (amask >> lane) & 1u;
-    uint64_t key = occ ? (((uint64_t)(uint32_t)sl.seq << 32) | (uint32_t)sl.idr) : ~0ULL;
     int rank = 0, pred = lane;
+    uint64_t key = occ ? (((uint64_t)(uint32_t)sl.seq << 32) | (uint32_t)sl.idr) : ~0ULL;
     uint64_t best = 0;
     for (uint32_t m = amask; m; m &= m - 1) {
         int j = __ffs((int)m) - 1;
@@ -1022,10 +1025,14 @@ __device__ __forceinline__ int scan_slots(const LutMem* L, uint32_t amask, int a
     double tcur = 0.0;
     adm = 0;
     mseq = 0;
+    double x = occ ? lut_eval(L, lut_rows_nb(L, rank + 1), cs) : 0.0;
+    const double smin = xsub((double)vmin, __shfl_sync(FULLMASK, x, __ffs((int)__ballot_sync(FULLMASK, occ && rank == an - 1)) - 1));
+    bool fresh = true;
     while (s < an) {
         bool valid = occ && rank >= s;
         int64_t bx = b + (rank - s) + 1;
-        double x = valid ? lut_eval(L, lut_rows_nb(L, bx), cs) : 0.0;
+        if (!fresh) x = valid ? lut_eval(L, lut_rows_nb(L, bx), cs) : 0.0;
+        fresh = false;
         double xprev = __shfl_sync(FULLMASK, x, pred);
         double tprev = rank == s ? tcur : xprev;
         int64_t bprev = bx - 1;
@@ -1272,15 +1279,13 @@ __device__ __noinline__ void simulate(const Ctx& cx, int64_t ii, const WS& w, in
                 if (DP == SLOSIM_DECODE_KAIROS_SLACK) {
                     dc_mask = 0;  // set below from the selection
                     // select_decode_batch decode_sched.py:60-111
-                    double fallback = lut_lookup(L, an, amax);
                     bool occ = (amask >> lane) & 1u;
                     int64_t v = occ ? tpot_slo * ((int64_t)(sl.seq - sl.inp) + 1) - (t - sl.tf) : SLOSIM_INF64;
-                    double smin = xsub((double)wmin64_redux(v), fallback);
                     uint32_t adm;
                     int64_t ms;
                     int b;
                     if (__builtin_expect(L->full, 1)) {
-                        b = scan_slots(L, amask, an, sl, smin, adm, ms, lane);
+                        b = scan_slots(L, amask, an, sl, wmin64_redux(v), adm, ms, lane);
                     } else {
                         // general LUT: memory-mode selection on a spilled copy
                         SIM_SYNC_OUT();
