@@ -5,6 +5,7 @@
 #include <cuda_runtime.h>
 #include <math.h>
 #include <stdio.h>
+#include <stdlib.h>
 #include <string.h>
 
 #include <algorithm>
@@ -62,6 +63,11 @@ int launch_geometry(int64_t n_instances, int* grid) {
         CK(cudaDeviceGetAttribute(&g_sms, cudaDevAttrMultiProcessorCount, dev));
         CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&g_blocks_per_sm, sim_kernel, 128, 0));
         if (g_blocks_per_sm < 1) g_blocks_per_sm = 1;
+        // experiment knob: fewer resident blocks per SM (occupancy studies)
+        if (const char* e = getenv("SLOSIM_BLOCKS_PER_SM")) {
+            int v = atoi(e);
+            if (v >= 1 && v < g_blocks_per_sm) g_blocks_per_sm = v;
+        }
     }
     int64_t warps_needed = n_instances;
     int64_t blocks = (warps_needed + 3) / 4;
@@ -795,3 +801,15 @@ extern "C" const char* slosim_build_info(void) {
 }
 
 extern "C" const char* slosim_last_error(void) { return g_err; }
+
+#ifdef SLOSIM_PROF
+// Debug builds only: read (and optionally reset) the section-profile counters of the engine loop.
+extern "C" int slosim_prof_read(unsigned long long* out16, int reset) {
+    CK(cudaMemcpyFromSymbol(out16, slosim::g_prof, 16 * sizeof(unsigned long long)));
+    if (reset) {
+        unsigned long long z[16] = {0};
+        CK(cudaMemcpyToSymbol(slosim::g_prof, z, sizeof(z)));
+    }
+    return 0;
+}
+#endif

@@ -498,6 +498,21 @@ struct Slot {
     int64_t tf;                                   // t_first_token
 };
 
+// Section profiling (debug builds with -DSLOSIM_PROF only): per-instance clock64
+// totals of the loop sections, summed over instances into g_prof (slosim_prof_read).
+#ifdef SLOSIM_PROF
+__device__ unsigned long long g_prof[16];
+#define PROF_DECL long long pf_acc[10] = {0, 0, 0, 0, 0, 0, 0, 0, 0, 0}; long long pf_t = clock64()
+#define PROF_MARK(k) do { long long pf_n = clock64(); pf_acc[k] += pf_n - pf_t; pf_t = pf_n; } while (0)
+#define PROF_COUNT(k, v) (pf_acc[k] += (v))
+#define PROF_FLUSH() do { if (lane == 0) for (int pk = 0; pk < 10; pk++) atomicAdd(&g_prof[pk], (unsigned long long)pf_acc[pk]); } while (0)
+#else
+#define PROF_DECL
+#define PROF_MARK(k)
+#define PROF_COUNT(k, v)
+#define PROF_FLUSH()
+#endif
+
 // 64-bit signed warp minimum from two 32-bit REDUX operations.
 __device__ __forceinline__ int64_t wmin64_redux(int64_t v) {
     int hi = (int)(v >> 32);
@@ -1006,6 +1021,7 @@ __device__ __noinline__ void on_decode_start_mem(Sim& S, int64_t t, int& bsz, in
 // The fallback cost lookup(|A|, max_seq) (decode_sched.py:75) is the first
 // round's evaluation of the last-ranked slot (|B| = an at its seq_len = max_seq),
 // so s_min = min(v) - that value is formed after the first evaluation.
+template <bool G>
 __device__ __forceinline__ int scan_slots(const LutMem* L, uint32_t amask, int an, const Slot& sl, int64_t vmin,
                                           uint32_t& adm, int64_t& mseq, int lane) {
     bool occ = (amask >> lane) & 1u;
@@ -1020,18 +1036,18 @@ __device__ __forceinline__ int scan_slots(const LutMem* L, uint32_t amask, int a
             if (kj >= best) { best = kj; pred = j; }
         }
     }
-    ColSel cs = lut_col(L, occ ? sl.seq : 1);
+    ColSel cs = lut_col<G>(L, occ ? sl.seq : 1);
     int b = 0, s = 0;
     double tcur = 0.0;
     adm = 0;
     mseq = 0;
-    double x = occ ? lut_eval(L, lut_rows_nb(L, rank + 1), cs) : 0.0;
+    double x = occ ? lut_eval<G>(L, lut_rows_nb<G>(L, rank + 1), cs) : 0.0;
     const double smin = xsub((double)vmin, __shfl_sync(FULLMASK, x, __ffs((int)__ballot_sync(FULLMASK, occ && rank == an - 1)) - 1));
     bool fresh = true;
     while (s < an) {
         bool valid = occ && rank >= s;
         int64_t bx = b + (rank - s) + 1;
-        if (!fresh) x = valid ? lut_eval(L, lut_rows_nb(L, bx), cs) : 0.0;
+        if (!fresh) x = valid ? lut_eval<G>(L, lut_rows_nb<G>(L, bx), cs) : 0.0;
         fresh = false;
         double xprev = __shfl_sync(FULLMASK, x, pred);
         double tprev = rank == s ? tcur : xprev;
@@ -1047,9 +1063,9 @@ __device__ __forceinline__ int scan_slots(const LutMem* L, uint32_t amask, int a
             s = f + 1;  // rank f is rejected under the now-current state
             continue;
         }
-        RowSel rs = lut_rows(L, b + 1);
+        RowSel rs = lut_rows<G>(L, b + 1);
         bool vy = occ && rank > s;
-        double y = vy ? lut_eval(L, rs, cs) : 0.0;
+        double y = vy ? lut_eval<G>(L, rs, cs) : 0.0;
         bool oky = vy && y <= smin && (b == 0 || quot_gt((double)(b + 1), y, (double)b, tcur));
         int g = __reduce_min_sync(FULLMASK, oky ? rank : an);
         if (g >= an) break;
@@ -1105,10 +1121,68 @@ __device__ __noinline__ int64_t on_retire(Sim& S, const Slot sl, int64_t t, bool
     return wsum64(kv_rel);
 }
 
+// Continuous batching between rare events (decode_sched.py:114-124 driven by
+// engine.py:377-413).  The batch is the whole active set, so consecutive decode
+// steps differ only in max_seq (+1 per step) until an arrival, transfer or
+// prefill completion arrives or a member retires.  Lane k evaluates the
+// ground-truth duration of the k-th step from now (k = 0: the step just
+// started), a warp scan gives the step end times, and the leading run of m
+// steps that end strictly before the next rare event with no member retiring
+// is applied in bulk: per-token deadlines (metrics.py:57-69) and the decision
+// digest, folded in step order.  Step m is left in progress exactly as the
+// loop would have started it.  Returns m (0: nothing applied).
+// Preconditions (checked by the caller): register mode, plain formula ground
+// truth, no per-step trace or LUT, no pending prefill start.
+__device__ __noinline__ int ff_continuous(Sim& S, Slot& sl, int64_t t, int lane) {
+    const bool occ = (S.amask >> lane) & 1u;
+    const int64_t ng = (int64_t)sl.seq - sl.inp;  // tokens generated before step 0
+    const int r = __reduce_min_sync(FULLMASK, occ ? (int)(sl.out - 2 - ng) : 0x7fffffff);
+    if (r < 1) return 0;
+    int64_t tr = S.next_arr;
+    tr = S.tr_min < tr ? S.tr_min : tr;
+    tr = S.pf_end < tr ? S.pf_end : tr;
+    const int64_t bsz = S.dc_bsz, bmax = S.dc_max;
+    const slosim_profile_t* P = S.P;
+    int64_t d = rint_i64(decode_formula(P->n_base, P->base_x, P->base_y, P->gamma, bsz, bmax + lane));
+    d = d < 1 ? 1 : d;
+    const int64_t e = t + wscan_incl64(d, lane);
+    // end times increase and r is a threshold, so the pure steps form a prefix
+    const int m = __popc(__ballot_sync(FULLMASK, e < tr && lane < r && lane < 31));
+    if (m == 0) return 0;
+    const uint32_t s = __reduce_add_sync(FULLMASK, occ ? member_hash((uint32_t)sl.pos) : 0u);
+    const uint64_t mid = ((uint64_t)s << 32) | (uint32_t)bsz;
+    const int64_t tpot = S.tpot_slo;
+    const int64_t c = sl.tf + ng * tpot;
+    uint64_t D = S.D;
+    int miss = 0;
+#pragma unroll 1
+    for (int k = 0; k < m; k++) {
+        const int64_t ek = __shfl_sync(FULLMASK, e, k);
+        const int64_t dk = __shfl_sync(FULLMASK, d, k);
+        miss += ek > c + (int64_t)(k + 1) * tpot;
+        D = dstep(D, (uint64_t)ek ^ 0x5A5A5A5A5A5A5A5AULL);
+        D = dstep(D, mid);
+        D = dstep(D, (uint64_t)dk);
+    }
+    if (occ) { sl.seq += m; sl.miss += miss; }
+    S.D = D;
+    S.dc_end = __shfl_sync(FULLMASK, e, m);
+    S.dc_dur = __shfl_sync(FULLMASK, d, m);
+    S.dc_max = bmax + m;
+    S.amax += m;
+    return m;
+}
+
+#ifdef SLOSIM_NO_SKIP1
+#define SKIP_SINGLE(an) true
+#else
+#define SKIP_SINGLE(an) ((an) > 1)
+#endif
+
 // DP: decode policy (compile-time), FULL: event trace / per-request rows / LUT
 // export compiled in.  The throughput path runs simulate<DP, false>, whose hot
 // loop carries no tracing or row-output code.
-template <int DP, bool FULL>
+template <int DP, bool FULL, bool G>
 __device__ __noinline__ void simulate(const Ctx& cx, int64_t ii, const WS& w, int lane) {
     const long long c0 = clock64();
     Sim S;
@@ -1172,6 +1246,7 @@ __device__ __noinline__ void simulate(const Ctx& cx, int64_t ii, const WS& w, in
     S.D = 0;
     Slot sl{0, 0, 0, 0, 0, 0, 0, 0};
     const int64_t tpot_slo = S.tpot_slo;
+    const bool gt_plain = S.P->gt_frozen == 0 && S.P->noise_eps <= 0.0;
 
     // hot state in registers; synced with S around the (rare) out-of-line calls
     int64_t next_arr, pf_end, dc_end, tr_min, dc_dur, dc_bsz, dc_max, amax, kv, t_end = 0;
@@ -1192,8 +1267,10 @@ __device__ __noinline__ void simulate(const Ctx& cx, int64_t ii, const WS& w, in
     S.qh = qh; S.qt = qt; S.ntps = ntps; S.finished = finished; S.amask = amask; S.dc_mask = dc_mask;          \
     S.regmode = regmode; S.D = D
     SIM_SYNC_IN();
+    PROF_DECL;
 
     for (;;) {
+        PROF_MARK(5);
         int64_t t = next_arr;
         t = pf_end < t ? pf_end : t;
         t = dc_end < t ? dc_end : t;
@@ -1209,6 +1286,7 @@ __device__ __noinline__ void simulate(const Ctx& cx, int64_t ii, const WS& w, in
             if (S.pf_end == t) on_prefill_done<FULL>(S, t, lane);
             SIM_SYNC_IN();
         }
+        PROF_MARK(0);
 
         // ---- decode step completion (engine.py:394-413): the hot path
         if (dc_end == t) {
@@ -1245,7 +1323,7 @@ __device__ __noinline__ void simulate(const Ctx& cx, int64_t ii, const WS& w, in
                 SIM_SYNC_IN();
             }
             if (use_lut) {
-                lut_update_warp(L, dc_bsz, dc_max, dc_dur, lane);
+                lut_update_warp<G>(L, dc_bsz, dc_max, dc_dur, lane);
                 __syncwarp();
             }
             dsteps++;
@@ -1260,6 +1338,7 @@ __device__ __noinline__ void simulate(const Ctx& cx, int64_t ii, const WS& w, in
             dc_end = SLOSIM_INF64;
         }
 
+        PROF_MARK(1);
         // admission, then a new prefill step (out of line)
         if (__builtin_expect(pt > ph || (pf_end == SLOSIM_INF64 && qt > qh), 0)) {
             SIM_SYNC_OUT();
@@ -1268,15 +1347,19 @@ __device__ __noinline__ void simulate(const Ctx& cx, int64_t ii, const WS& w, in
             SIM_SYNC_IN();
         }
 
+        PROF_MARK(2);
         // ---- start a decode step (engine.py:377-392): the hot path
         if (dc_end == SLOSIM_INF64 && an > 0) {
+            PROF_COUNT(7, an == 1);
             v_dec += an;
             max_a = an > max_a ? an : max_a;
             int bsz = an;
             int64_t bmax = amax;
             if (__builtin_expect(regmode, 1)) {
                 dc_mask = amask;
-                if (DP == SLOSIM_DECODE_KAIROS_SLACK) {
+                // With one active request both outcomes of Alg. 3 (admit it, or fall
+                // back to the whole active set) are the same batch: skip the scan.
+                if (DP == SLOSIM_DECODE_KAIROS_SLACK && SKIP_SINGLE(an)) {
                     dc_mask = 0;  // set below from the selection
                     // select_decode_batch decode_sched.py:60-111
                     bool occ = (amask >> lane) & 1u;
@@ -1285,7 +1368,7 @@ __device__ __noinline__ void simulate(const Ctx& cx, int64_t ii, const WS& w, in
                     int64_t ms;
                     int b;
                     if (__builtin_expect(L->full, 1)) {
-                        b = scan_slots(L, amask, an, sl, wmin64_redux(v), adm, ms, lane);
+                        b = scan_slots<G>(L, amask, an, sl, wmin64_redux(v), adm, ms, lane);
                     } else {
                         // general LUT: memory-mode selection on a spilled copy
                         SIM_SYNC_OUT();
@@ -1313,7 +1396,7 @@ __device__ __noinline__ void simulate(const Ctx& cx, int64_t ii, const WS& w, in
             // _GroundTruth.decode_step_us engine.py:185-192 (frozen profiles and noise out of line)
             const slosim_profile_t* P = S.P;
             double val;
-            if (__builtin_expect(P->gt_frozen == 0 && P->noise_eps <= 0.0, 1))
+            if (__builtin_expect(gt_plain, 1))
                 val = decode_formula(P->n_base, P->base_x, P->base_y, P->gamma, bsz, bmax);
             else
                 val = gt_decode_cold(S, cx.frozen_tab + pid, bsz, bmax);
@@ -1322,8 +1405,26 @@ __device__ __noinline__ void simulate(const Ctx& cx, int64_t ii, const WS& w, in
             dc_bsz = bsz;
             dc_max = bmax;
             dc_end = t + dc_dur;
+#ifndef SLOSIM_NO_FF
+            if (DP == SLOSIM_DECODE_CONTINUOUS && !use_lut && regmode && gt_plain && !(FULL && S.T.buf) &&
+                dc_end < next_arr && dc_end < tr_min && dc_end < pf_end &&
+                !(pf_end == SLOSIM_INF64 && qt > qh)) {
+                PROF_MARK(3);
+                SIM_SYNC_OUT();
+                const int m = ff_continuous(S, sl, t, lane);
+                SIM_SYNC_IN();
+                PROF_MARK(4);
+                PROF_COUNT(8, 1);
+                PROF_COUNT(9, m);
+                dsteps += m;
+                v_dec += (int64_t)m * an;
+                b_dec += (int64_t)m * bsz;
+            }
+#endif
         }
+        PROF_MARK(3);
     }
+    PROF_FLUSH();
     SIM_SYNC_OUT();
 #undef SIM_SYNC_IN
 #undef SIM_SYNC_OUT
@@ -1352,13 +1453,28 @@ __global__ void __launch_bounds__(128, SLOSIM_MIN_BLOCKS)
         k = __shfl_sync(FULLMASK, k, 0);
         if ((int64_t)k >= N) break;
         const int64_t ii = cx.B.order ? cx.B.order[k] : (int64_t)k;
-        const bool kairos = cx.B.instances[ii].decode_policy == SLOSIM_DECODE_KAIROS_SLACK;
+        const slosim_instance_t* I = cx.B.instances + ii;
+        const bool kairos = I->decode_policy == SLOSIM_DECODE_KAIROS_SLACK;
+        // power-of-two LUT geometry: index arithmetic and exact power-of-two divisions
+#ifdef SLOSIM_NO_GEO
+        const bool geo = false;
+#else
+        const bool geo = cx.sched_tab[I->profile_id].geo != 0;
+#endif
         if (full) {
-            if (kairos) simulate<SLOSIM_DECODE_KAIROS_SLACK, true>(cx, ii, w, lane);
-            else simulate<SLOSIM_DECODE_CONTINUOUS, true>(cx, ii, w, lane);
+            if (kairos) {
+                if (geo) simulate<SLOSIM_DECODE_KAIROS_SLACK, true, true>(cx, ii, w, lane);
+                else simulate<SLOSIM_DECODE_KAIROS_SLACK, true, false>(cx, ii, w, lane);
+            } else {
+                simulate<SLOSIM_DECODE_CONTINUOUS, true, false>(cx, ii, w, lane);
+            }
         } else {
-            if (kairos) simulate<SLOSIM_DECODE_KAIROS_SLACK, false>(cx, ii, w, lane);
-            else simulate<SLOSIM_DECODE_CONTINUOUS, false>(cx, ii, w, lane);
+            if (kairos) {
+                if (geo) simulate<SLOSIM_DECODE_KAIROS_SLACK, false, true>(cx, ii, w, lane);
+                else simulate<SLOSIM_DECODE_KAIROS_SLACK, false, false>(cx, ii, w, lane);
+            } else {
+                simulate<SLOSIM_DECODE_CONTINUOUS, false, false>(cx, ii, w, lane);
+            }
         }
         __syncwarp();
     }

@@ -33,6 +33,8 @@ struct LutMem {
     int32_t nb, ns, sshift, full;
     uint32_t rowmask;
     int32_t populated;
+    int32_t geo;  // 1: bsz buckets 2^0..2^(nb-1) and seq buckets (j+1) << wsh (index math, no tables)
+    int32_t wsh;
     uint8_t bidx[264];  // bidx[b] = bisect_left(bb, b), b <= 256
     uint8_t sidx[264];  // sidx[q] = bisect_left(sb, q << sshift), q <= 256
 };
@@ -121,10 +123,17 @@ __device__ void lut_build(LutMem* L, int nb, int ns, const int32_t* bb, const in
     for (int c = lane; c < nb * ns; c += 32) cells += L->cnt[c] > 0;
 #pragma unroll
     for (int o = 16; o; o >>= 1) cells += __shfl_xor_sync(0xffffffffu, cells, o);
+    int wsh = 0;
+    while (wsh < 30 && (1 << wsh) < sb[0]) wsh++;
+    bool geo = nb <= 16 && (1 << wsh) == sb[0];
+    for (int i = 0; i < nb; i++) geo = geo && bb[i] == (1 << i);
+    for (int j = 0; j < ns; j++) geo = geo && (int64_t)sb[j] == ((int64_t)(j + 1) << wsh);
     if (lane == 0) {
         L->rowmask = rm;
         L->populated = cells;
         L->full = cells == nb * ns;
+        L->geo = geo ? 1 : 0;
+        L->wsh = wsh;
     }
     __syncwarp();
 }
@@ -144,17 +153,40 @@ __device__ void lut_copy(LutMem* dst, const LutMem* src, int lane) {
     if (lane == 0) {
         dst->nb = src->nb; dst->ns = src->ns; dst->sshift = src->sshift; dst->full = src->full;
         dst->rowmask = src->rowmask; dst->populated = src->populated;
+        dst->geo = src->geo; dst->wsh = src->wsh;
     }
     __syncwarp();
 }
 
 // ---- full-grid fast path ----------------------------------------------------
+// G = true: the power-of-two geometry (L->geo; the reference's default buckets
+// costmodel.py:26-27 are of this shape).  Bucket indices are then integer
+// arithmetic, and every divisor of the interpolations (b_hi - b_lo = 2^k across
+// rows, the seq bucket width 2^wsh along a row) is a power of two, so the
+// correctly rounded quotient is the exact product with 2^-k: same bits, one
+// DMUL instead of a DDIV.
 struct ColSel { int c; double dx; };   // value of a row = slope[row][c]*dx + mean[row][c]
-struct RowSel { int r1, r2; int64_t num, den; };  // r2 < 0: single row r1
+struct RowSel { int r1, r2; int64_t num, den; double inv; };  // r2 < 0: single row r1; inv = 1/den (G)
+
+__device__ __forceinline__ double pow2_neg(int k) { return __longlong_as_double((long long)(1023 - k) << 52); }
+
+// bisect_left over the geometry: smallest i with 2^i >= b (b >= 1), smallest j with (j+1) << wsh >= s (s >= 1)
+__device__ __forceinline__ int geo_bidx(int64_t b) { return b <= 1 ? 0 : 64 - __clzll((long long)(b - 1)); }
+__device__ __forceinline__ int geo_sidx(const LutMem* L, int64_t s) {
+    return (int)(((s + ((int64_t)1 << L->wsh) - 1) >> L->wsh) - 1);
+}
 
 // np.interp column selection (numpy arr_interp) for a fully populated row.
+template <bool G = false>
 __device__ __forceinline__ ColSel lut_col(const LutMem* L, int64_t seq) {
     int ns = L->ns;
+    if (G) {
+        // c = floor(seq / W) - 1 and dx = seq mod W inside the grid (dx = 0 at a node), clamped outside
+        const int w = L->wsh;
+        int64_t c = (seq >> w) - 1;
+        bool in = seq > ((int64_t)1 << w) && c < ns - 1;
+        return ColSel{in ? (int)c : (seq <= ((int64_t)1 << w) ? 0 : ns - 1), in ? (double)(seq & (((int64_t)1 << w) - 1)) : 0.0};
+    }
     if (seq <= (int64_t)L->sb[0]) return ColSel{0, 0.0};
     if (seq >= (int64_t)L->sb[ns - 1]) return ColSel{ns - 1, 0.0};
     int j0 = lut_sidx(L, seq);
@@ -163,31 +195,53 @@ __device__ __forceinline__ ColSel lut_col(const LutMem* L, int64_t seq) {
 }
 
 // Row selection of lookup() (costmodel.py:175-187) when every row is populated.
+template <bool G = false>
 __device__ __forceinline__ RowSel lut_rows(const LutMem* L, int64_t bsz) {
+    if (G) {
+        int i = geo_bidx(bsz);
+        if (i == 0) return RowSel{0, -1, 0, 1, 1.0};
+        if (i >= L->nb) return RowSel{L->nb - 1, -1, 0, 1, 1.0};
+        if (((int64_t)1 << i) == bsz) return RowSel{i, -1, 0, 1, 1.0};
+        return RowSel{i - 1, i, bsz - ((int64_t)1 << (i - 1)), (int64_t)1 << (i - 1), pow2_neg(i - 1)};
+    }
     int i = lut_bidx(L, bsz);
-    if (i == 0) return RowSel{0, -1, 0, 1};
-    if (i == L->nb) return RowSel{L->nb - 1, -1, 0, 1};
-    if ((int64_t)L->bb[i] == bsz) return RowSel{i, -1, 0, 1};
-    return RowSel{i - 1, i, bsz - L->bb[i - 1], (int64_t)L->bb[i] - L->bb[i - 1]};
+    if (i == 0) return RowSel{0, -1, 0, 1, 1.0};
+    if (i == L->nb) return RowSel{L->nb - 1, -1, 0, 1, 1.0};
+    if ((int64_t)L->bb[i] == bsz) return RowSel{i, -1, 0, 1, 1.0};
+    return RowSel{i - 1, i, bsz - L->bb[i - 1], (int64_t)L->bb[i] - L->bb[i - 1], 1.0};
 }
 
 // Branch-free row selection for per-lane batch sizes (speculative scan).
+template <bool G = false>
 __device__ __forceinline__ RowSel lut_rows_nb(const LutMem* L, int64_t bsz) {
-    int i = lut_bidx(L, bsz);
     int nb = L->nb;
+    RowSel rs;
+    if (G) {
+        int i = geo_bidx(bsz);
+        bool single = (i == 0) | (i >= nb) | (((int64_t)1 << i) == bsz);
+        int lo = i >= nb ? nb - 1 : (i == 0 ? 0 : i - 1);
+        rs.r1 = single ? (i >= nb ? nb - 1 : i) : lo;
+        rs.r2 = single ? -1 : i;
+        rs.num = single ? 0 : bsz - ((int64_t)1 << lo);
+        rs.den = single ? 1 : (int64_t)1 << lo;
+        rs.inv = pow2_neg(single ? 0 : lo);
+        return rs;
+    }
+    int i = lut_bidx(L, bsz);
     int ic = i < nb ? i : nb - 1;
     int64_t bi = L->bb[ic];
     bool single = (i == 0) | (i == nb) | (bi == bsz);
     int r1 = i == 0 ? 0 : (i == nb ? nb - 1 : (bi == bsz ? i : i - 1));
     int64_t blo = L->bb[r1];
-    RowSel rs;
     rs.r1 = r1;
     rs.r2 = single ? -1 : i;
     rs.num = single ? 0 : bsz - blo;
     rs.den = single ? 1 : bi - blo;
+    rs.inv = 1.0;
     return rs;
 }
 
+template <bool G = false>
 __device__ __forceinline__ double lut_eval(const LutMem* L, const RowSel& rs, const ColSel& cs) {
     int ns = L->ns;
     int k1 = rs.r1 * ns + cs.c;
@@ -196,6 +250,7 @@ __device__ __forceinline__ double lut_eval(const LutMem* L, const RowSel& rs, co
     int k2 = rs.r2 * ns + cs.c;
     double v2 = xadd(xmul(L->slope[k2], cs.dx), L->mean[k2]);
     // v_lo + (v_hi - v_lo) * (bsz - b_lo) / (b_hi - b_lo)
+    if (G) return xadd(v1, xmul(xmul(xsub(v2, v1), (double)rs.num), rs.inv));
     return xadd(v1, xdiv(xmul(xsub(v2, v1), (double)rs.num), (double)rs.den));
 }
 
@@ -267,13 +322,14 @@ __device__ __noinline__ void lut_update(LutMem* L, int64_t bsz, int64_t max_seq,
 // cell mean and the np.interp slopes into and out of the cell concurrently
 // (neighbouring columns are the populated neighbours); otherwise lane 0 runs
 // the general update.
+template <bool G = false>
 __device__ __forceinline__ void lut_update_warp(LutMem* L, int64_t bsz, int64_t max_seq, int64_t obs, int lane) {
     if (!L->full) {
         if (lane == 0) lut_update(L, bsz, max_seq, obs);
         return;
     }
-    int i = lut_bidx(L, bsz), j = lut_sidx(L, max_seq);
     const int nb = L->nb, ns = L->ns;
+    int i = G ? geo_bidx(bsz) : lut_bidx(L, bsz), j = G ? geo_sidx(L, max_seq) : lut_sidx(L, max_seq);
     i = i < nb - 1 ? i : nb - 1;
     j = j < ns - 1 ? j : ns - 1;
     const int c = i * ns + j;
@@ -287,7 +343,8 @@ __device__ __forceinline__ void lut_update_warp(LutMem* L, int64_t bsz, int64_t 
         int a = right ? j : j - 1;
         double ma = right ? mean : L->mean[c - 1];
         double mb = right ? L->mean[c + 1] : mean;
-        L->slope[i * ns + a] = xdiv(xsub(mb, ma), xsub((double)L->sb[a + 1], (double)L->sb[a]));
+        L->slope[i * ns + a] = G ? xmul(xsub(mb, ma), pow2_neg(L->wsh))
+                                 : xdiv(xsub(mb, ma), xsub((double)L->sb[a + 1], (double)L->sb[a]));
     }
 }
 
