@@ -459,6 +459,12 @@ __device__ void write_config_error(slosim_summary_t* out, int n) {
 }
 
 // ------------------------------------------------------ instance state --
+// One active decode request held in a lane's registers (engine.py:374 _active).
+struct Slot {
+    int32_t pos, seq, idr, out, inp, miss, flag;  // flag bit1: TTFT met
+    int64_t tf;                                   // t_first_token
+};
+
 // All per-instance state of one simulation.  It lives in registers inside the
 // hot decode loop of simulate(); the rare per-request events (arrival,
 // transfer, prefill completion/start, admission) are out-of-line functions
@@ -490,13 +496,15 @@ struct Sim {
     uint64_t D;
     TraceW T;
     Pcg64 rng;  // decode noise (engine.py:191), drawn only when noise_eps > 0
+    // the lane's slot, handed to out-of-line code by reference; the hot loop
+    // keeps its own copy in registers (never address-taken)
+    Slot sl;
+    // results of the memory-mode decode handlers
+    int sel_bsz, sel_nmem;
+    int64_t sel_max;
+    uint32_t sel_hash;
 };
 
-// One active decode request held in a lane's registers (engine.py:374 _active).
-struct Slot {
-    int32_t pos, seq, idr, out, inp, miss, flag;  // flag bit1: TTFT met
-    int64_t tf;                                   // t_first_token
-};
 
 // Section profiling (debug builds with -DSLOSIM_PROF only): per-instance clock64
 // totals of the loop sections, summed over instances into g_prof (slosim_prof_read).
@@ -894,8 +902,9 @@ __device__ __noinline__ void on_finalize(Sim& S, long long c0, int lane) {
 
 // ---- memory-mode decode step completion (> 32 active; engine.py:394-413)
 template <bool FULL>
-__device__ __noinline__ void on_decode_done_mem(Sim& S, Slot& sl, int64_t t, uint32_t& s_out, int& nmem_out,
-                                               int lane) {
+__device__ __noinline__ void on_decode_done_mem(Sim& S, Slot& sl, int64_t t, int lane) {
+    uint32_t& s_out = S.sel_hash;
+    int& nmem_out = S.sel_nmem;
     const WS& w = S.w;
     int32_t* a_pos = w.i32(A_POS);
     int32_t* a_seq = w.i32(A_SEQ);
@@ -983,9 +992,11 @@ __device__ __noinline__ void on_decode_done_mem(Sim& S, Slot& sl, int64_t t, uin
 
 // ---- memory-mode decode start (> 32 active; engine.py:377-392, decode_sched.py:60-124)
 template <int DP>
-__device__ __noinline__ void on_decode_start_mem(Sim& S, int64_t t, int& bsz, int64_t& bmax, int lane) {
+__device__ __noinline__ void on_decode_start_mem(Sim& S, int64_t t, int lane) {
     const WS& w = S.w;
     const int an = S.an;
+    int& bsz = S.sel_bsz;
+    int64_t& bmax = S.sel_max;
     bsz = an;
     bmax = S.amax;
     S.dc_prefix = an;
@@ -1121,19 +1132,28 @@ __device__ __noinline__ int64_t on_retire(Sim& S, const Slot sl, int64_t t, bool
     return wsum64(kv_rel);
 }
 
-// Continuous batching between rare events (decode_sched.py:114-124 driven by
-// engine.py:377-413).  The batch is the whole active set, so consecutive decode
-// steps differ only in max_seq (+1 per step) until an arrival, transfer or
-// prefill completion arrives or a member retires.  Lane k evaluates the
-// ground-truth duration of the k-th step from now (k = 0: the step just
-// started), a warp scan gives the step end times, and the leading run of m
-// steps that end strictly before the next rare event with no member retiring
-// is applied in bulk: per-token deadlines (metrics.py:57-69) and the decision
-// digest, folded in step order.  Step m is left in progress exactly as the
-// loop would have started it.  Returns m (0: nothing applied).
+// Decode steps between rare events, applied in bulk.  Under continuous
+// batching (decode_sched.py:114-124) the batch is the whole active set; under
+// Alg. 3 with a single active request it is that request whatever the scan
+// decides.  Either way consecutive decode steps (engine.py:377-413) differ
+// only in max_seq (+1 per step) until an arrival, transfer or prefill
+// completion arrives or a member retires.  Lane k evaluates the ground-truth
+// duration of the k-th step from now (k = 0: the step just started), a warp
+// scan gives the step end times, and the leading run of m steps that end
+// strictly before the next rare event with no member retiring is applied at
+// once: per-token deadlines (metrics.py:57-69) and the decision digest, folded
+// in step order, and (LUTUPD) the m DecodeStepLUT.update calls
+// (costmodel.py:118-128).  Nothing reads the LUT inside the run, and the m
+// steps are kept to one cell, so the updates collapse into one: the cell sum
+// grows by the exact integer total (the cell sum must be an integer below
+// 2^53, so every intermediate f64 sum is exact in any grouping), the count by
+// m, and the mean and slopes are recomputed once from the final sums.  Step m
+// is left in progress exactly as the loop would have started it.  Returns m.
 // Preconditions (checked by the caller): register mode, plain formula ground
-// truth, no per-step trace or LUT, no pending prefill start.
-__device__ __noinline__ int ff_continuous(Sim& S, Slot& sl, int64_t t, int lane) {
+// truth, no per-step trace, no pending prefill start; LUTUPD: one active
+// request and a fully populated LUT.
+template <bool LUTUPD, bool G>
+__device__ __noinline__ int ff_steps(Sim& S, Slot& sl, int64_t t, int lane) {
     const bool occ = (S.amask >> lane) & 1u;
     const int64_t ng = (int64_t)sl.seq - sl.inp;  // tokens generated before step 0
     const int r = __reduce_min_sync(FULLMASK, occ ? (int)(sl.out - 2 - ng) : 0x7fffffff);
@@ -1146,9 +1166,30 @@ __device__ __noinline__ int ff_continuous(Sim& S, Slot& sl, int64_t t, int lane)
     int64_t d = rint_i64(decode_formula(P->n_base, P->base_x, P->base_y, P->gamma, bsz, bmax + lane));
     d = d < 1 ? 1 : d;
     const int64_t e = t + wscan_incl64(d, lane);
-    // end times increase and r is a threshold, so the pure steps form a prefix
-    const int m = __popc(__ballot_sync(FULLMASK, e < tr && lane < r && lane < 31));
+    bool pure = e < tr && lane < r && lane < 31;
+    LutMem* L = S.L;
+    if (LUTUPD) {
+        // the LUT cell of step k (bucket of (bsz, max_seq)); j is nondecreasing in k
+        const int ns = L->ns;
+        int j = G ? geo_sidx(L, bmax + lane) : lut_sidx(L, bmax + lane);
+        j = j < ns - 1 ? j : ns - 1;
+        const int j0 = __shfl_sync(FULLMASK, j, 0);  // unconditional: every lane takes part
+        pure = pure && j == j0;
+    }
+    // end times increase and the other bounds are thresholds, so the pure steps form a prefix
+    const int m = __popc(__ballot_sync(FULLMASK, pure));
     if (m == 0) return 0;
+    if (LUTUPD) {
+        const int64_t dsum = wsum64(lane < m ? d : 0);
+        const int nb = L->nb, ns = L->ns;
+        int i = G ? geo_bidx(bsz) : lut_bidx(L, bsz), j = G ? geo_sidx(L, bmax) : lut_sidx(L, bmax);
+        i = i < nb - 1 ? i : nb - 1;
+        j = j < ns - 1 ? j : ns - 1;
+        const double s0 = L->sum[i * ns + j];
+        if (!(s0 == rint(s0) && fabs(s0) + (double)dsum < 0x1p53)) return 0;
+        lut_update_warp<G>(L, bsz, bmax, dsum, lane, m);
+        __syncwarp();
+    }
     const uint32_t s = __reduce_add_sync(FULLMASK, occ ? member_hash((uint32_t)sl.pos) : 0u);
     const uint64_t mid = ((uint64_t)s << 32) | (uint32_t)bsz;
     const int64_t tpot = S.tpot_slo;
@@ -1172,6 +1213,12 @@ __device__ __noinline__ int ff_continuous(Sim& S, Slot& sl, int64_t t, int lane)
     S.amax += m;
     return m;
 }
+
+#ifdef SLOSIM_NO_FF_KAIROS
+#define FF_KAIROS false
+#else
+#define FF_KAIROS true
+#endif
 
 #ifdef SLOSIM_NO_SKIP1
 #define SKIP_SINGLE(an) true
@@ -1319,7 +1366,11 @@ __device__ __noinline__ void simulate(const Ctx& cx, int64_t ii, const WS& w, in
                 an = __popc(amask);
             } else {
                 SIM_SYNC_OUT();
-                on_decode_done_mem<FULL>(S, sl, t, s, nmem, lane);
+                S.sl = sl;
+                on_decode_done_mem<FULL>(S, S.sl, t, lane);
+                sl = S.sl;
+                s = S.sel_hash;
+                nmem = S.sel_nmem;
                 SIM_SYNC_IN();
             }
             if (use_lut) {
@@ -1342,7 +1393,11 @@ __device__ __noinline__ void simulate(const Ctx& cx, int64_t ii, const WS& w, in
         // admission, then a new prefill step (out of line)
         if (__builtin_expect(pt > ph || (pf_end == SLOSIM_INF64 && qt > qh), 0)) {
             SIM_SYNC_OUT();
-            if (S.pt > S.ph) on_admit<FULL>(S, sl, t, lane);
+            if (S.pt > S.ph) {
+                S.sl = sl;
+                on_admit<FULL>(S, S.sl, t, lane);
+                sl = S.sl;
+            }
             if (S.pf_end == SLOSIM_INF64 && S.qt > S.qh) on_prefill_start<FULL>(S, t, lane);
             SIM_SYNC_IN();
         }
@@ -1372,8 +1427,11 @@ __device__ __noinline__ void simulate(const Ctx& cx, int64_t ii, const WS& w, in
                     } else {
                         // general LUT: memory-mode selection on a spilled copy
                         SIM_SYNC_OUT();
-                        to_memory_mode(S, sl, lane);
-                        on_decode_start_mem<DP>(S, t, bsz, bmax, lane);
+                        S.sl = sl;
+                        to_memory_mode(S, S.sl, lane);
+                        on_decode_start_mem<DP>(S, t, lane);
+                        bsz = S.sel_bsz;
+                        bmax = S.sel_max;
                         // map the flag bits back to slots (slot order == compacted order)
                         int d = __popc(amask & lanemask_lt(lane));
                         bool f = ((amask >> lane) & 1u) && (S.w.i32(A_FLAG)[d] & 1);
@@ -1389,8 +1447,10 @@ __device__ __noinline__ void simulate(const Ctx& cx, int64_t ii, const WS& w, in
                 }
             } else {
                 SIM_SYNC_OUT();
-                on_decode_start_mem<DP>(S, t, bsz, bmax, lane);
+                on_decode_start_mem<DP>(S, t, lane);
                 SIM_SYNC_IN();
+                bsz = S.sel_bsz;
+                bmax = S.sel_max;
             }
             b_dec += bsz;
             // _GroundTruth.decode_step_us engine.py:185-192 (frozen profiles and noise out of line)
@@ -1406,12 +1466,15 @@ __device__ __noinline__ void simulate(const Ctx& cx, int64_t ii, const WS& w, in
             dc_max = bmax;
             dc_end = t + dc_dur;
 #ifndef SLOSIM_NO_FF
-            if (DP == SLOSIM_DECODE_CONTINUOUS && !use_lut && regmode && gt_plain && !(FULL && S.T.buf) &&
-                dc_end < next_arr && dc_end < tr_min && dc_end < pf_end &&
+            if ((DP == SLOSIM_DECODE_CONTINUOUS ? !use_lut : (FF_KAIROS && an == 1 && L->full != 0)) && regmode &&
+                gt_plain && !(FULL && S.T.buf) && dc_end < next_arr && dc_end < tr_min && dc_end < pf_end &&
                 !(pf_end == SLOSIM_INF64 && qt > qh)) {
                 PROF_MARK(3);
                 SIM_SYNC_OUT();
-                const int m = ff_continuous(S, sl, t, lane);
+                S.sl = sl;
+                const int m = DP == SLOSIM_DECODE_CONTINUOUS ? ff_steps<false, false>(S, S.sl, t, lane)
+                                                             : ff_steps<true, G>(S, S.sl, t, lane);
+                sl = S.sl;
                 SIM_SYNC_IN();
                 PROF_MARK(4);
                 PROF_COUNT(8, 1);

@@ -323,7 +323,8 @@ __device__ __noinline__ void lut_update(LutMem* L, int64_t bsz, int64_t max_seq,
 // (neighbouring columns are the populated neighbours); otherwise lane 0 runs
 // the general update.
 template <bool G = false>
-__device__ __forceinline__ void lut_update_warp(LutMem* L, int64_t bsz, int64_t max_seq, int64_t obs, int lane) {
+__device__ __forceinline__ void lut_update_warp(LutMem* L, int64_t bsz, int64_t max_seq, int64_t obs, int lane,
+                                                int32_t add = 1) {
     if (!L->full) {
         if (lane == 0) lut_update(L, bsz, max_seq, obs);
         return;
@@ -334,7 +335,7 @@ __device__ __forceinline__ void lut_update_warp(LutMem* L, int64_t bsz, int64_t 
     j = j < ns - 1 ? j : ns - 1;
     const int c = i * ns + j;
     double sum = xadd(L->sum[c], (double)obs);
-    int32_t cnt = L->cnt[c] + 1;
+    int32_t cnt = L->cnt[c] + add;
     double mean = xdiv(sum, (double)cnt);
     // lane 0: the cell; lane 1: slope (j -> j+1); lane 2: slope (j-1 -> j)
     if (lane == 0) { L->sum[c] = sum; L->cnt[c] = cnt; L->mean[c] = mean; }

@@ -27,7 +27,10 @@ for k in range(1, STEPS + 1):
     ms.append(e0.elapsed_time(e1))
 h = db.summaries.cpu().numpy().view(_abi.summary_dtype())
 np.save(OUT, h)
-print(json.dumps({"ms": ms, "mreq_s": SL * 1000 / (sum(ms) / len(ms)) / 1e3}))
+cyc = h["sim_cycles"].astype(np.float64)
+pair = np.arange(len(h)) % 4
+by = [float(cyc[(pair == p) & (np.arange(len(h)) >= STEPS * SL)].sum()) for p in range(4)]
+print(json.dumps({"ms": ms, "mreq_s": SL * 1000 / (sum(ms) / len(ms)) / 1e3, "gcyc_by_pair_last": [round(x / 1e9, 2) for x in by]}))
 '''
 
 res = {}
@@ -54,4 +57,5 @@ for spec in sys.argv[1:]:
         if bad:
             r["mismatch"] = bad
     res[name] = r
-    print(f"{name:14s} {r['mreq_s']:7.3f} M req/s  ms={['%.1f' % x for x in r['ms']]}  exact={r['exact']}", flush=True)
+    print(f"{name:14s} {r['mreq_s']:7.3f} M req/s  ms={['%.1f' % x for x in r['ms']]}  exact={r['exact']}  "
+          f"warp Gcycles by pair (last slice) {r['gcyc_by_pair_last']}", flush=True)
