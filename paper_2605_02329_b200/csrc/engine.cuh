@@ -1090,6 +1090,87 @@ __device__ __forceinline__ int scan_slots(const LutMem* L, uint32_t amask, int a
     return b;
 }
 
+// quot_gt (numerics.cuh) split for the hot scan: the product test decides
+// unless the two products are within 2^-50 of each other (`tie`), in which
+// case the caller divides exactly out of line.
+__device__ __forceinline__ bool quot_gt_fast(double a, double x, double b, double y, bool& tie) {
+    const double p = __dmul_rn(a, y), q = __dmul_rn(b, x);
+    const bool gt = p > __dmul_rn(q, 1.0 + 0x1p-50);
+    tie = !gt && !(p < __dmul_rn(q, 1.0 - 0x1p-50));
+    return gt;
+}
+__device__ __noinline__ bool quot_gt_exact(double a, double x, double b, double y) {
+    return __ddiv_rn(a, x) > __ddiv_rn(b, y);
+}
+
+// scan_slots on the power-of-two geometry (the benchmark's hot path), same
+// decisions with fewer dependent steps: ranks are found two slots per
+// iteration, and every round evaluates both hypotheses (X: the run from rank s
+// on is admitted; Y: state unchanged) so that a round resolves with one
+// uniform branch whichever applies.
+__device__ __forceinline__ int scan_geo(const LutMem* L, const Geo& g, uint32_t amask, int an, const Slot& sl,
+                                        int64_t vmin, uint32_t& adm, int& mseq, int lane) {
+    const bool occ = (amask >> lane) & 1u;
+    const uint64_t key = occ ? (((uint64_t)(uint32_t)sl.seq << 32) | (uint32_t)sl.idr) : ~0ULL;
+    int rank = 0, pred = lane;
+    uint64_t best = 0;
+    for (uint32_t m = amask; m;) {
+        const int j1 = __ffs((int)m) - 1;
+        m &= m - 1;
+        const int j2 = m ? __ffs((int)m) - 1 : j1;
+        m &= m - 1;
+        const uint64_t k1 = __shfl_sync(FULLMASK, key, j1), k2 = __shfl_sync(FULLMASK, key, j2);
+        const bool l1 = k1 < key, l2 = k2 < key && j2 != j1;
+        rank += (int)l1 + (int)l2;
+        if (l1 && k1 >= best) { best = k1; pred = j1; }
+        if (l2 && k2 >= best) { best = k2; pred = j2; }
+    }
+    const ColSel cs = gcol(g, occ ? sl.seq : 1);
+    int b = 0, s = 0;
+    double tcur = 0.0;
+    adm = 0;
+    mseq = 0;
+    double x = geval(L, g, grows(g, rank + 1), cs);
+    const int llast = __ffs((int)__ballot_sync(FULLMASK, occ && rank == an - 1)) - 1;
+    const double smin = xsub((double)vmin, __shfl_sync(FULLMASK, x, llast));
+    bool first = true;
+    for (;;) {
+        const bool valid = occ && rank >= s;
+        const int bx = b + (rank - s) + 1;
+        if (!first) x = geval(L, g, grows(g, bx), cs);
+        first = false;
+        const double y = geval(L, g, grows(g, b + 1), cs);
+        const double xprev = __shfl_sync(FULLMASK, x, pred);
+        const double tprev = rank == s ? tcur : xprev;
+        const int bprev = bx - 1;
+        bool tx, ty;
+        bool qx = quot_gt_fast((double)(bprev + 1), x, (double)bprev, tprev, tx);
+        bool qy = quot_gt_fast((double)(b + 1), y, (double)b, tcur, ty);
+        const bool vy = occ && rank > s;
+        const bool ex = valid && x <= smin && bprev != 0 && tx;
+        const bool ey = vy && y <= smin && b != 0 && ty;
+        if (__any_sync(FULLMASK, ex || ey)) {
+            if (ex) qx = quot_gt_exact((double)(bprev + 1), x, (double)bprev, tprev);
+            if (ey) qy = quot_gt_exact((double)(b + 1), y, (double)b, tcur);
+        }
+        const bool okx = valid && x <= smin && (bprev == 0 || qx);
+        const bool oky = vy && y <= smin && (b == 0 || qy);
+        const int f = __reduce_min_sync(FULLMASK, (valid && !okx) ? rank : an);
+        const int gy = __reduce_min_sync(FULLMASK, oky ? rank : an);
+        const bool run = f > s;
+        if (!run && gy >= an) break;  // Y admits nothing: the window is rejected
+        const int last = run ? f - 1 : gy;
+        const int ll = __ffs((int)__ballot_sync(FULLMASK, occ && rank == last)) - 1;
+        adm |= __ballot_sync(FULLMASK, occ && (run ? (rank >= s && rank < f) : rank == gy));
+        tcur = __shfl_sync(FULLMASK, run ? x : y, ll);
+        mseq = __shfl_sync(FULLMASK, sl.seq, ll);
+        b += run ? f - s : 1;
+        s = last + (run ? 2 : 1);  // X: rank f is rejected under the new state
+        if (s >= an) break;
+    }
+    return b;
+}
+
 // Ground-truth decode step for frozen (file-backed) profiles and/or noise
 // (engine.py:185-192): out of the hot loop, which then carries neither the
 // general LUT lookup nor the PCG64 state.
@@ -1229,8 +1310,13 @@ __device__ __noinline__ int ff_steps(Sim& S, Slot& sl, int64_t t, int lane) {
 // DP: decode policy (compile-time), FULL: event trace / per-request rows / LUT
 // export compiled in.  The throughput path runs simulate<DP, false>, whose hot
 // loop carries no tracing or row-output code.
+#ifdef SLOSIM_SIM_NOINLINE
+#define SIM_INLINE __noinline__
+#else
+#define SIM_INLINE __forceinline__
+#endif
 template <int DP, bool FULL, bool G>
-__device__ __noinline__ void simulate(const Ctx& cx, int64_t ii, const WS& w, int lane) {
+__device__ SIM_INLINE void simulate(const Ctx& cx, int64_t ii, const WS& w, int lane) {
     const long long c0 = clock64();
     Sim S;
     S.B = &cx.B;
@@ -1272,6 +1358,8 @@ __device__ __noinline__ void simulate(const Ctx& cx, int64_t ii, const WS& w, in
     S.L = w.lut();
     LutMem* L = S.L;
     if (use_lut) lut_copy(L, ST, lane);
+    bool lut_full = use_lut && L->full != 0;
+    const Geo geo = G ? geo_of(ST) : Geo{0, 0, 0};
     S.est_tok = S.P->est_tokens;
     S.est_busy = S.P->est_busy_us;
     S.rng = Pcg64{I->rng_state_hi, I->rng_state_lo, I->rng_inc_hi, I->rng_inc_lo};
@@ -1340,16 +1428,14 @@ __device__ __noinline__ void simulate(const Ctx& cx, int64_t ii, const WS& w, in
             uint32_t s = 0;
             int nmem = 0;
             if (__builtin_expect(regmode, 1)) {
-                bool inb = (dc_mask >> lane) & 1u;
-                bool retire = false;
-                uint32_t hsh = 0;
-                if (inb) {
-                    sl.seq += 1;
-                    int64_t ngen = sl.seq - sl.inp;
-                    hsh = member_hash((uint32_t)sl.pos);
-                    if (t > sl.tf + ngen * tpot_slo) sl.miss++;  // deadline_misses metrics.py:57-69
-                    retire = ngen == sl.out - 1;
-                }
+                // branch-free member update: token time, per-token deadline
+                // (deadline_misses metrics.py:57-69), retirement test
+                const bool inb = (dc_mask >> lane) & 1u;
+                sl.seq += inb ? 1 : 0;
+                const int ngen = sl.seq - sl.inp;
+                const uint32_t hsh = inb ? member_hash((uint32_t)sl.pos) : 0u;
+                sl.miss += (inb && t > sl.tf + (int64_t)ngen * tpot_slo) ? 1 : 0;
+                const bool retire = inb && ngen == sl.out - 1;
                 unsigned rmask = __ballot_sync(FULLMASK, retire);
                 if (__builtin_expect(rmask != 0, 0)) {
                     kv -= on_retire<FULL>(S, sl, t, retire, ntps, lane);
@@ -1374,8 +1460,14 @@ __device__ __noinline__ void simulate(const Ctx& cx, int64_t ii, const WS& w, in
                 SIM_SYNC_IN();
             }
             if (use_lut) {
-                lut_update_warp<G>(L, dc_bsz, dc_max, dc_dur, lane);
-                __syncwarp();
+                if (G && lut_full) {
+                    gupdate(L, geo, (int)dc_bsz, (int)dc_max, dc_dur, lane);
+                    __syncwarp();
+                } else {
+                    lut_update_warp<G>(L, dc_bsz, dc_max, dc_dur, lane);
+                    __syncwarp();
+                    lut_full = L->full != 0;
+                }
             }
             dsteps++;
             D = dstep(D, (uint64_t)t ^ 0x5A5A5A5A5A5A5A5AULL);
@@ -1422,7 +1514,11 @@ __device__ __noinline__ void simulate(const Ctx& cx, int64_t ii, const WS& w, in
                     uint32_t adm;
                     int64_t ms;
                     int b;
-                    if (__builtin_expect(L->full, 1)) {
+                    if (G && __builtin_expect(lut_full, 1)) {
+                        int msq;
+                        b = scan_geo(L, geo, amask, an, sl, wmin64_redux(v), adm, msq, lane);
+                        ms = msq;
+                    } else if (__builtin_expect(lut_full, 1)) {
                         b = scan_slots<G>(L, amask, an, sl, wmin64_redux(v), adm, ms, lane);
                     } else {
                         // general LUT: memory-mode selection on a spilled copy
@@ -1466,7 +1562,7 @@ __device__ __noinline__ void simulate(const Ctx& cx, int64_t ii, const WS& w, in
             dc_max = bmax;
             dc_end = t + dc_dur;
 #ifndef SLOSIM_NO_FF
-            if ((DP == SLOSIM_DECODE_CONTINUOUS ? !use_lut : (FF_KAIROS && an == 1 && L->full != 0)) && regmode &&
+            if ((DP == SLOSIM_DECODE_CONTINUOUS ? !use_lut : (FF_KAIROS && an == 1 && lut_full)) && regmode &&
                 gt_plain && !(FULL && S.T.buf) && dc_end < next_arr && dc_end < tr_min && dc_end < pf_end &&
                 !(pf_end == SLOSIM_INF64 && qt > qh)) {
                 PROF_MARK(3);

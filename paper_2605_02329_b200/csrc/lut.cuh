@@ -254,6 +254,74 @@ __device__ __forceinline__ double lut_eval(const LutMem* L, const RowSel& rs, co
     return xadd(v1, xdiv(xmul(xsub(v2, v1), (double)rs.num), (double)rs.den));
 }
 
+// ---- power-of-two geometry, hot-loop forms ----------------------------------
+// The same arithmetic as lut_col/lut_rows_nb/lut_eval/lut_update_warp<true>,
+// with the instance-invariant geometry held in registers (Geo), 32-bit
+// indices, both rows always loaded (no branch on a single row) and the cell
+// update written branch-free with predicated stores.
+struct Geo { int nb, ns, wsh; };
+__device__ __forceinline__ Geo geo_of(const LutMem* L) { return Geo{L->nb, L->ns, L->wsh}; }
+__device__ __forceinline__ int gbidx(int b) { return b <= 1 ? 0 : 32 - __clz(b - 1); }
+
+__device__ __forceinline__ ColSel gcol(const Geo& g, int seq) {
+    const int w = 1 << g.wsh;
+    const int c = (seq >> g.wsh) - 1;
+    const bool in = seq > w && c < g.ns - 1;
+    return ColSel{in ? c : (seq <= w ? 0 : g.ns - 1), in ? (double)(seq & (w - 1)) : 0.0};
+}
+
+__device__ __forceinline__ RowSel grows(const Geo& g, int bsz) {
+    const int i = gbidx(bsz);
+    const bool single = (i == 0) | (i >= g.nb) | ((1u << i) == (unsigned)bsz);
+    const int lo = i >= g.nb ? g.nb - 1 : (i == 0 ? 0 : i - 1);
+    RowSel rs;
+    rs.r1 = single ? (i >= g.nb ? g.nb - 1 : i) : lo;
+    rs.r2 = single ? -1 : i;
+    rs.num = single ? 0 : bsz - (1 << lo);
+    rs.den = single ? 1 : (1 << lo);
+    rs.inv = pow2_neg(single ? 0 : lo);
+    return rs;
+}
+
+__device__ __forceinline__ double geval(const LutMem* L, const Geo& g, const RowSel& rs, const ColSel& cs) {
+    const int k1 = rs.r1 * g.ns + cs.c;
+    const int k2 = (rs.r2 < 0 ? rs.r1 : rs.r2) * g.ns + cs.c;
+    const double v1 = xadd(xmul(L->slope[k1], cs.dx), L->mean[k1]);
+    const double v2 = xadd(xmul(L->slope[k2], cs.dx), L->mean[k2]);
+    const double r = xadd(v1, xmul(xmul(xsub(v2, v1), (double)rs.num), rs.inv));
+    return rs.r2 < 0 ? v1 : r;
+}
+
+__device__ __forceinline__ void st_if(bool p, double* a, double v) {
+    asm volatile("{\n\t.reg .pred q;\n\tsetp.ne.u32 q, %0, 0;\n\t@q st.f64 [%1], %2;\n\t}" ::"r"((unsigned)p), "l"(a),
+                 "d"(v) : "memory");
+}
+__device__ __forceinline__ void st_if(bool p, int32_t* a, int32_t v) {
+    asm volatile("{\n\t.reg .pred q;\n\tsetp.ne.u32 q, %0, 0;\n\t@q st.s32 [%1], %2;\n\t}" ::"r"((unsigned)p), "l"(a),
+                 "r"(v) : "memory");
+}
+
+// DecodeStepLUT.update (costmodel.py:118-128) on a full power-of-two grid:
+// lane 0 writes the cell, lane 1 the slope out of it, lane 2 the slope into it.
+// The neighbour mean is loaded by every lane (cells c-1 and c+1 always lie
+// inside the LutMem block) and only the stores are predicated.
+__device__ __forceinline__ void gupdate(LutMem* L, const Geo& g, int bsz, int max_seq, int64_t obs, int lane,
+                                        int32_t add = 1) {
+    const int i = min(gbidx(bsz), g.nb - 1);
+    const int j = min(((max_seq + (1 << g.wsh) - 1) >> g.wsh) - 1, g.ns - 1);
+    const int c = i * g.ns + j;
+    const double sum = xadd(L->sum[c], (double)obs);
+    const int32_t cnt = L->cnt[c] + add;
+    const double mean = xdiv(sum, (double)cnt);
+    const bool right = lane == 1 && j + 1 < g.ns, left = lane == 2 && j > 0;
+    const double mn = L->mean[lane == 1 ? c + 1 : c - 1];
+    const double ma = right ? mean : mn, mb = right ? mn : mean;
+    st_if(lane == 0, &L->sum[c], sum);
+    st_if(lane == 0, &L->cnt[c], cnt);
+    st_if(lane == 0, &L->mean[c], mean);
+    st_if(right || left, &L->slope[right ? c : c - 1], xmul(xsub(mb, ma), pow2_neg(g.wsh)));
+}
+
 // ---- general path -----------------------------------------------------------
 // np.interp(seq, xs, ys) over the populated columns of row r; j0 = bisect_left(sb, seq).
 __device__ __forceinline__ double lut_row_eval(const LutMem* L, int r, int64_t seq, int j0) {
