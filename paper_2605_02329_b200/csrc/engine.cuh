@@ -1108,11 +1108,20 @@ __device__ __noinline__ bool quot_gt_exact(double a, double x, double b, double 
 // iteration, and every round evaluates both hypotheses (X: the run from rank s
 // on is admitted; Y: state unchanged) so that a round resolves with one
 // uniform branch whichever applies.
+// The (seq_len, id) ranks of the previous step are kept (rk_rank, rk_pred for
+// the occupied-lane set rk_mask) and reused when the slot set is unchanged and
+// every slot still compares above its rank predecessor: the old rank order is
+// then still sorted, so the ranks are unchanged.
 __device__ __forceinline__ int scan_geo(const LutMem* L, const Geo& g, uint32_t amask, int an, const Slot& sl,
-                                        int64_t vmin, uint32_t& adm, int& mseq, int lane) {
+                                        int64_t vmin, uint32_t& adm, int& mseq, int& rk_rank, int& rk_pred,
+                                        uint32_t& rk_mask, int lane) {
     const bool occ = (amask >> lane) & 1u;
     const uint64_t key = occ ? (((uint64_t)(uint32_t)sl.seq << 32) | (uint32_t)sl.idr) : ~0ULL;
-    int rank = 0, pred = lane;
+    int rank = rk_rank, pred = rk_pred;
+    const uint64_t kp = __shfl_sync(FULLMASK, key, pred);
+    if (rk_mask != amask || __any_sync(FULLMASK, occ && rank > 0 && !(kp < key))) {
+    rank = 0;
+    pred = lane;
     uint64_t best = 0;
     for (uint32_t m = amask; m;) {
         const int j1 = __ffs((int)m) - 1;
@@ -1124,6 +1133,10 @@ __device__ __forceinline__ int scan_geo(const LutMem* L, const Geo& g, uint32_t 
         rank += (int)l1 + (int)l2;
         if (l1 && k1 >= best) { best = k1; pred = j1; }
         if (l2 && k2 >= best) { best = k2; pred = j2; }
+    }
+    rk_rank = rank;
+    rk_pred = pred;
+    rk_mask = amask;
     }
     const ColSel cs = gcol(g, occ ? sl.seq : 1);
     int b = 0, s = 0;
@@ -1359,6 +1372,8 @@ __device__ SIM_INLINE void simulate(const Ctx& cx, int64_t ii, const WS& w, int 
     LutMem* L = S.L;
     if (use_lut) lut_copy(L, ST, lane);
     bool lut_full = use_lut && L->full != 0;
+    int rk_rank = 0, rk_pred = lane;  // cached slot ranks of the kairos scan (scan_geo)
+    uint32_t rk_mask = 0;
     const Geo geo = G ? geo_of(ST) : Geo{0, 0, 0};
     S.est_tok = S.P->est_tokens;
     S.est_busy = S.P->est_busy_us;
@@ -1382,39 +1397,50 @@ __device__ SIM_INLINE void simulate(const Ctx& cx, int64_t ii, const WS& w, int 
     Slot sl{0, 0, 0, 0, 0, 0, 0, 0};
     const int64_t tpot_slo = S.tpot_slo;
     const bool gt_plain = S.P->gt_frozen == 0 && S.P->noise_eps <= 0.0;
+    // one- or two-anchor ground-truth decode curve staged in shared memory (per warp)
+    __shared__ GtLine gt_lines[4];
+    GtLine* const gtl = gt_lines + (threadIdx.x >> 5);
+    bool gt_fast = false;
+    if (lane == 0) gt_fast = gt_line_make(S.P->n_base, S.P->base_x, S.P->base_y, S.P->gamma, *gtl);
+    gt_fast = __shfl_sync(FULLMASK, gt_fast, 0);
+    __syncwarp();
 
-    // hot state in registers; synced with S around the (rare) out-of-line calls
-    int64_t next_arr, pf_end, dc_end, tr_min, dc_dur, dc_bsz, dc_max, amax, kv, t_end = 0;
-    int an, ph, pt, qh, qt, ntps, finished;
+    // hot state in registers; synced with S around the (rare) out-of-line calls.
+    // The rare-event clocks (next arrival, prefill end, first transfer) and the
+    // queue/pending cursors change only inside those calls, so the hot loop
+    // keeps just their minimum (t_rare) and two derived flags.
+    int64_t dc_end, dc_dur, dc_bsz, dc_max, amax, kv, t_end = 0;
+    int64_t t_rare;
+    bool adm_pend, pf_wait;
+    int an, ntps, finished;
     uint32_t amask, dc_mask;
     bool regmode;
     uint64_t D;
     int64_t dsteps = 0, v_dec = 0, b_dec = 0;
     int32_t max_a = 0;
 #define SIM_SYNC_IN()                                                                                          \
-    next_arr = S.next_arr; pf_end = S.pf_end; dc_end = S.dc_end; tr_min = S.tr_min; dc_dur = S.dc_dur;       \
-    dc_bsz = S.dc_bsz; dc_max = S.dc_max; amax = S.amax; kv = S.kv; an = S.an; ph = S.ph; pt = S.pt;          \
-    qh = S.qh; qt = S.qt; ntps = S.ntps; finished = S.finished; amask = S.amask; dc_mask = S.dc_mask;          \
-    regmode = S.regmode; D = S.D
+    dc_end = S.dc_end; dc_dur = S.dc_dur; dc_bsz = S.dc_bsz; dc_max = S.dc_max; amax = S.amax; kv = S.kv;     \
+    an = S.an; ntps = S.ntps; finished = S.finished; amask = S.amask; dc_mask = S.dc_mask;                    \
+    regmode = S.regmode; D = S.D;                                                                              \
+    t_rare = S.next_arr < S.pf_end ? S.next_arr : S.pf_end;                                                    \
+    t_rare = S.tr_min < t_rare ? S.tr_min : t_rare;                                                            \
+    adm_pend = S.pt > S.ph;                                                                                    \
+    pf_wait = S.pf_end == SLOSIM_INF64 && S.qt > S.qh
 #define SIM_SYNC_OUT()                                                                                         \
-    S.next_arr = next_arr; S.pf_end = pf_end; S.dc_end = dc_end; S.tr_min = tr_min; S.dc_dur = dc_dur;       \
-    S.dc_bsz = dc_bsz; S.dc_max = dc_max; S.amax = amax; S.kv = kv; S.an = an; S.ph = ph; S.pt = pt;          \
-    S.qh = qh; S.qt = qt; S.ntps = ntps; S.finished = finished; S.amask = amask; S.dc_mask = dc_mask;          \
+    S.dc_end = dc_end; S.dc_dur = dc_dur; S.dc_bsz = dc_bsz; S.dc_max = dc_max; S.amax = amax; S.kv = kv;     \
+    S.an = an; S.ntps = ntps; S.finished = finished; S.amask = amask; S.dc_mask = dc_mask;                    \
     S.regmode = regmode; S.D = D
     SIM_SYNC_IN();
     PROF_DECL;
 
     for (;;) {
         PROF_MARK(5);
-        int64_t t = next_arr;
-        t = pf_end < t ? pf_end : t;
-        t = dc_end < t ? dc_end : t;
-        t = tr_min < t ? tr_min : t;
+        const int64_t t = dc_end < t_rare ? dc_end : t_rare;
         if (t == SLOSIM_INF64) break;
         t_end = t;
 
         // rare events (a few per request) run out of line, in the reference's order
-        if (__builtin_expect(next_arr == t || tr_min == t || pf_end == t, 0)) {
+        if (__builtin_expect(t_rare == t, 0)) {
             SIM_SYNC_OUT();
             if (S.next_arr == t) on_arrivals<FULL>(S, t, lane);
             if (S.tr_min == t) on_transfers<FULL>(S, t, lane);
@@ -1483,7 +1509,7 @@ __device__ SIM_INLINE void simulate(const Ctx& cx, int64_t ii, const WS& w, int 
 
         PROF_MARK(1);
         // admission, then a new prefill step (out of line)
-        if (__builtin_expect(pt > ph || (pf_end == SLOSIM_INF64 && qt > qh), 0)) {
+        if (__builtin_expect(adm_pend || pf_wait, 0)) {
             SIM_SYNC_OUT();
             if (S.pt > S.ph) {
                 S.sl = sl;
@@ -1516,7 +1542,8 @@ __device__ SIM_INLINE void simulate(const Ctx& cx, int64_t ii, const WS& w, int 
                     int b;
                     if (G && __builtin_expect(lut_full, 1)) {
                         int msq;
-                        b = scan_geo(L, geo, amask, an, sl, wmin64_redux(v), adm, msq, lane);
+                        b = scan_geo(L, geo, amask, an, sl, wmin64_redux(v), adm, msq, rk_rank, rk_pred, rk_mask,
+                                     lane);
                         ms = msq;
                     } else if (__builtin_expect(lut_full, 1)) {
                         b = scan_slots<G>(L, amask, an, sl, wmin64_redux(v), adm, ms, lane);
@@ -1552,7 +1579,9 @@ __device__ SIM_INLINE void simulate(const Ctx& cx, int64_t ii, const WS& w, int 
             // _GroundTruth.decode_step_us engine.py:185-192 (frozen profiles and noise out of line)
             const slosim_profile_t* P = S.P;
             double val;
-            if (__builtin_expect(gt_plain, 1))
+            if (__builtin_expect(gt_plain && gt_fast, 1))
+                val = gt_line_eval(*gtl, bsz, bmax);
+            else if (gt_plain)
                 val = decode_formula(P->n_base, P->base_x, P->base_y, P->gamma, bsz, bmax);
             else
                 val = gt_decode_cold(S, cx.frozen_tab + pid, bsz, bmax);
@@ -1562,9 +1591,9 @@ __device__ SIM_INLINE void simulate(const Ctx& cx, int64_t ii, const WS& w, int 
             dc_max = bmax;
             dc_end = t + dc_dur;
 #ifndef SLOSIM_NO_FF
-            if ((DP == SLOSIM_DECODE_CONTINUOUS ? !use_lut : (FF_KAIROS && an == 1 && lut_full)) && regmode &&
-                gt_plain && !(FULL && S.T.buf) && dc_end < next_arr && dc_end < tr_min && dc_end < pf_end &&
-                !(pf_end == SLOSIM_INF64 && qt > qh)) {
+            if ((DP == SLOSIM_DECODE_CONTINUOUS ? !use_lut : (FF_KAIROS && an == 1)) &&
+                (DP == SLOSIM_DECODE_CONTINUOUS || lut_full) && regmode && gt_plain && !(FULL && S.T.buf) &&
+                dc_end < t_rare && !pf_wait) {
                 PROF_MARK(3);
                 SIM_SYNC_OUT();
                 S.sl = sl;

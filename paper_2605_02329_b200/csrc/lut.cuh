@@ -433,6 +433,24 @@ __device__ __forceinline__ double decode_formula(int n, const int64_t* bx, const
     return xmul(interp_clamped(n, bx, by, seq), xadd(1.0, xmul(gamma, (double)(bsz - 1))));
 }
 
+// decode_step_formula for the (common) one- or two-anchor base curve, with
+// the anchors staged once per instance (shared memory in the engine): the same
+// expression as interp_clamped + decode_formula, without the anchor search.
+struct GtLine { double y0, y1, dy, dx, gamma; int64_t x0, x1; };
+__device__ __forceinline__ bool gt_line_make(int n, const int64_t* bx, const double* by, double gamma, GtLine& k) {
+    if (n < 1 || n > 2) return false;
+    k.x0 = bx[0]; k.x1 = bx[n - 1]; k.y0 = by[0]; k.y1 = by[n - 1];
+    k.dy = xsub(k.y1, k.y0);
+    k.dx = (double)(k.x1 - k.x0);
+    k.gamma = gamma;
+    return true;
+}
+__device__ __forceinline__ double gt_line_eval(const GtLine& k, int64_t bsz, int64_t seq) {
+    const double mid = xadd(k.y0, xdiv(xmul(k.dy, (double)(seq - k.x0)), k.dx));
+    const double base = seq <= k.x0 ? k.y0 : (seq >= k.x1 ? k.y1 : mid);
+    return xmul(base, xadd(1.0, xmul(k.gamma, (double)(bsz - 1))));
+}
+
 // _GroundTruth._curve_at engine.py:161-173 (integer points; int + int*int/int).
 __device__ __forceinline__ double curve_at(int n, const int64_t* x, const int64_t* y, int64_t tokens) {
     if (tokens >= x[n - 1]) {
