@@ -342,15 +342,17 @@ def measure_e2e(args, sw, timed, slice_n, world):
     pk = sw.packed
     pin = lambda a: torch.from_numpy(np.array(a, copy=True)).pin_memory().numpy()
     arr, inp, out, hit, idr = pin(pk.arrival), pin(pk.inp), pin(pk.out), pin(pk.hit), pin(pk.idr)
-    times, reqs, h2d, d2h = [], 0, 0, 0
+    times, reqs, h2d, d2h, kernel_ms = [], 0, 0, 0, []
     for s in timed:
         inst = pin(pk.instances[s * slice_n:(s + 1) * slice_n].view(np.uint8)).view(_abi.instance_dtype())
         part = PackedBatch(arr, inp, out, hit, idr, pk.profiles, inst, 0, 0, 0)
         part.summaries = pin(part.summaries.view(np.uint8)).view(_abi.summary_dtype())
         b = part.host_struct()
+        kms = ctypes.c_float(0)
         t0 = time.perf_counter()
-        rc = _abi.lib().slosim_run_batch_host(ctypes.byref(b), None)
+        rc = _abi.lib().slosim_run_batch_host(ctypes.byref(b), ctypes.byref(kms))
         times.append(time.perf_counter() - t0)
+        kernel_ms.append(round(kms.value, 1))
         assert rc == 0
         reqs += part.n_requests
         h2d = arr.nbytes + inp.nbytes + out.nbytes + hit.nbytes + idr.nbytes + ctypes.sizeof(pk.profiles) + inst.nbytes
@@ -363,7 +365,8 @@ def measure_e2e(args, sw, timed, slice_n, world):
     if dist.is_available() and dist.is_initialized():
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
     return {"value": reqs * world / float(t.item()), "unit": "simulated requests/s", "h2d_bytes_per_step": h2d,
-            "d2h_bytes_per_step": d2h, "entry_point": "slosim_run_batch_host (C-ABI, host buffers)"}
+            "d2h_bytes_per_step": d2h, "entry_point": "slosim_run_batch_host (C-ABI, host buffers)",
+            "wall_ms_per_step": [round(x * 1e3, 1) for x in times], "kernel_ms_per_step": kernel_ms}
 
 
 def cpu_baseline(args, host_summ, slice_id, slice_n):

@@ -129,33 +129,34 @@ extern "C" int slosim_run_batch(const slosim_batch_t* b, void* stream) {
 }
 
 namespace {
-template <class T>
-cudaError_t up(T** d, const T* h, size_t n, std::vector<void*>& owned) {
-    *d = nullptr;
-    if (!h || n == 0) return cudaSuccess;
-    cudaError_t e = cudaMalloc((void**)d, n * sizeof(T));
-    if (e != cudaSuccess) return e;
-    owned.push_back(*d);
-    return cudaMemcpy(*d, h, n * sizeof(T), cudaMemcpyHostToDevice);
-}
-template <class T>
-cudaError_t alloc(T** d, size_t n, std::vector<void*>& owned) {
-    *d = nullptr;
-    if (n == 0) return cudaSuccess;
-    cudaError_t e = cudaMalloc((void**)d, n * sizeof(T));
-    if (e == cudaSuccess) owned.push_back(*d);
-    return e;
-}
-struct Owned {
-    std::vector<void*> v;
-    ~Owned() { for (void* p : v) cudaFree(p); }
+// Device staging for the host-buffer entry point: one grow-only arena carved
+// into 256-byte-aligned pieces (no cudaMalloc/cudaFree per call, so a call
+// costs its copies and kernels only).
+Arena g_io;
+std::mutex g_io_mu;
+struct Carve {
+    char* base = nullptr;
+    size_t off = 0;
+    template <class T>
+    T* take(size_t n) {
+        if (n == 0) return nullptr;
+        T* p = base ? (T*)(base + off) : nullptr;
+        off += (n * sizeof(T) + 255) & ~(size_t)255;
+        return p;
+    }
 };
+template <class T>
+cudaError_t up(T* d, const T* h, size_t n) {
+    if (!d || !h || n == 0) return cudaSuccess;
+    return cudaMemcpyAsync(d, h, n * sizeof(T), cudaMemcpyHostToDevice, 0);
+}
 }  // namespace
 
 // Default processing order of the persistent work queue (same rule as
-// batch.schedule_order): group by decode policy (slack-guided first) so each
-// SM runs one specialised engine loop at a time, longest-first inside a group
-// (cost = n_requests x arrival stretch factor).
+// batch.schedule_order): group by decode policy (slack-guided first), then by
+// prefill policy, so each SM runs one specialised engine loop and prefill
+// handler at a time; longest-first inside a group (cost = n_requests x
+// arrival stretch factor).
 static void default_order(const slosim_batch_t* hb, std::vector<int64_t>& order) {
     size_t n = (size_t)hb->n_instances;
     order.resize(n);
@@ -168,13 +169,15 @@ static void default_order(const slosim_batch_t* hb, std::vector<int64_t>& order)
     std::stable_sort(order.begin(), order.end(), [&](int64_t a, int64_t b) {
         int da = hb->instances[a].decode_policy, db = hb->instances[b].decode_policy;
         if (da != db) return da > db;
+        int pa = hb->instances[a].prefill_policy, pb = hb->instances[b].prefill_policy;
+        if (pa != pb) return pa > pb;
         return cost[a] > cost[b];
     });
 }
 
 extern "C" int slosim_run_batch_host(const slosim_batch_t* hb, float* elapsed_ms) {
     if (!hb) return SLOSIM_EINVAL;
-    Owned o;
+    std::lock_guard<std::mutex> lock(g_io_mu);
     slosim_batch_t d = *hb;
     size_t nt = (size_t)hb->traces.n_total, ni = (size_t)hb->n_instances;
     int64_t rows_n = 0, tb_n = 0;
@@ -184,57 +187,84 @@ extern "C" int slosim_run_batch_host(const slosim_batch_t* hb, float* elapsed_ms
         if (x.trace_buf_offset >= 0) tb_n = std::max<int64_t>(tb_n, x.trace_buf_offset + x.trace_buf_words);
         d.max_requests = std::max<int64_t>(d.max_requests, x.n_requests);
     }
-    CK(up((int64_t**)&d.traces.arrival_us, hb->traces.arrival_us, nt, o.v));
-    CK(up((int32_t**)&d.traces.input_len, hb->traces.input_len, nt, o.v));
-    CK(up((int32_t**)&d.traces.output_len, hb->traces.output_len, nt, o.v));
-    CK(up((int32_t**)&d.traces.prefix_hit_len, hb->traces.prefix_hit_len, nt, o.v));
-    CK(up((int32_t**)&d.traces.id_rank, hb->traces.id_rank, nt, o.v));
-    CK(up((slosim_profile_t**)&d.profiles, hb->profiles, (size_t)hb->n_profiles, o.v));
-    CK(up((slosim_instance_t**)&d.instances, hb->instances, ni, o.v));
-    CK(alloc(&d.summaries, ni, o.v));
-    bool rows = (hb->flags & SLOSIM_F_ROWS) != 0;
-    size_t rn = rows ? (size_t)rows_n : 0;
-    CK(alloc(&d.rows.ttft_us, rn, o.v)); CK(alloc(&d.rows.mean_tpot_us, rn, o.v));
-    CK(alloc(&d.rows.decode_tps, rn, o.v)); CK(alloc(&d.rows.met_flags, rn, o.v));
-    CK(alloc(&d.rows.deadline_misses, rn, o.v)); CK(alloc(&d.rows.t_prefill_finish, rn, o.v));
-    CK(alloc(&d.rows.t_first_token, rn, o.v)); CK(alloc(&d.rows.t_last_token, rn, o.v));
-    CK(alloc(&d.rows.first_sched_us, rn, o.v));
-    size_t tbn = hb->trace_buf ? (size_t)tb_n : 0;
-    CK(alloc(&d.trace_buf, tbn, o.v));
-    if (!hb->trace_buf) d.trace_buf = nullptr;
+    const bool rows = (hb->flags & SLOSIM_F_ROWS) != 0;
+    const size_t rn = rows ? (size_t)rows_n : 0;
+    const size_t tbn = hb->trace_buf ? (size_t)tb_n : 0;
     const size_t FR = SLOSIM_MAX_BSZ_BUCKETS * SLOSIM_MAX_SEQ_BUCKETS;
-    bool lut = (hb->flags & SLOSIM_F_EXPORT_LUT) && hb->lut_out_sums;
-    CK(alloc(&d.lut_out_sums, lut ? ni * FR : 0, o.v));
-    CK(alloc(&d.lut_out_counts, lut ? ni * FR : 0, o.v));
+    const bool lut = (hb->flags & SLOSIM_F_EXPORT_LUT) && hb->lut_out_sums;
     std::vector<int64_t> order;
     if (hb->order) order.assign(hb->order, hb->order + ni);
     else default_order(hb, order);
-    CK(up((int64_t**)&d.order, order.data(), ni, o.v));
+    // pass 0 sizes the arena, pass 1 carves it
+    for (int pass = 0; pass < 2; pass++) {
+        Carve c;
+        if (pass == 1) {
+            CK(g_io.reserve(0));
+            c.base = (char*)g_io.ptr;
+        }
+        d.traces.arrival_us = c.take<int64_t>(nt);
+        d.traces.input_len = c.take<int32_t>(nt);
+        d.traces.output_len = c.take<int32_t>(nt);
+        d.traces.prefix_hit_len = c.take<int32_t>(nt);
+        d.traces.id_rank = c.take<int32_t>(nt);
+        d.profiles = c.take<slosim_profile_t>((size_t)hb->n_profiles);
+        d.instances = c.take<slosim_instance_t>(ni);
+        d.summaries = c.take<slosim_summary_t>(ni);
+        d.rows.ttft_us = c.take<int64_t>(rn);
+        d.rows.mean_tpot_us = c.take<double>(rn);
+        d.rows.decode_tps = c.take<double>(rn);
+        d.rows.met_flags = c.take<uint8_t>(rn);
+        d.rows.deadline_misses = c.take<int32_t>(rn);
+        d.rows.t_prefill_finish = c.take<int64_t>(rn);
+        d.rows.t_first_token = c.take<int64_t>(rn);
+        d.rows.t_last_token = c.take<int64_t>(rn);
+        d.rows.first_sched_us = c.take<int64_t>(rn);
+        d.trace_buf = c.take<int64_t>(tbn);
+        d.lut_out_sums = c.take<double>(lut ? ni * FR : 0);
+        d.lut_out_counts = c.take<int32_t>(lut ? ni * FR : 0);
+        d.order = c.take<int64_t>(ni);
+        if (pass == 0) CK(g_io.reserve(c.off));
+    }
+    CK(up((int64_t*)d.traces.arrival_us, hb->traces.arrival_us, nt));
+    CK(up((int32_t*)d.traces.input_len, hb->traces.input_len, nt));
+    CK(up((int32_t*)d.traces.output_len, hb->traces.output_len, nt));
+    CK(up((int32_t*)d.traces.prefix_hit_len, hb->traces.prefix_hit_len, nt));
+    CK(up((int32_t*)d.traces.id_rank, hb->traces.id_rank, nt));
+    CK(up((slosim_profile_t*)d.profiles, hb->profiles, (size_t)hb->n_profiles));
+    CK(up((slosim_instance_t*)d.instances, hb->instances, ni));
+    CK(up((int64_t*)d.order, order.data(), ni));
+    if (!hb->trace_buf) d.trace_buf = nullptr;
     cudaEvent_t e0, e1;
     CK(cudaEventCreate(&e0));
     CK(cudaEventCreate(&e1));
     CK(cudaEventRecord(e0, 0));
     int rc = slosim_run_batch(&d, nullptr);
     CK(cudaEventRecord(e1, 0));
-    CK(cudaEventSynchronize(e1));
-    if (elapsed_ms) cudaEventElapsedTime(elapsed_ms, e0, e1);
-    cudaEventDestroy(e0);
-    cudaEventDestroy(e1);
-    if (rc) return rc;
-    CK(cudaMemcpy(hb->summaries, d.summaries, ni * sizeof(slosim_summary_t), cudaMemcpyDeviceToHost));
+    if (rc) {
+        cudaEventSynchronize(e1);
+        cudaEventDestroy(e0);
+        cudaEventDestroy(e1);
+        return rc;
+    }
+    CK(cudaMemcpyAsync(hb->summaries, d.summaries, ni * sizeof(slosim_summary_t), cudaMemcpyDeviceToHost, 0));
     if (rows) {
         const slosim_rows_t& R = hb->rows;
-#define COPYROW(f, T) if (R.f) CK(cudaMemcpy(R.f, d.rows.f, rn * sizeof(T), cudaMemcpyDeviceToHost))
+#define COPYROW(f, T) \
+    if (R.f) CK(cudaMemcpyAsync(R.f, d.rows.f, rn * sizeof(T), cudaMemcpyDeviceToHost, 0))
         COPYROW(ttft_us, int64_t); COPYROW(mean_tpot_us, double); COPYROW(decode_tps, double);
         COPYROW(met_flags, uint8_t); COPYROW(deadline_misses, int32_t); COPYROW(t_prefill_finish, int64_t);
         COPYROW(t_first_token, int64_t); COPYROW(t_last_token, int64_t); COPYROW(first_sched_us, int64_t);
 #undef COPYROW
     }
-    if (tbn) CK(cudaMemcpy(hb->trace_buf, d.trace_buf, tbn * sizeof(int64_t), cudaMemcpyDeviceToHost));
+    if (tbn) CK(cudaMemcpyAsync(hb->trace_buf, d.trace_buf, tbn * sizeof(int64_t), cudaMemcpyDeviceToHost, 0));
     if (lut) {
-        CK(cudaMemcpy(hb->lut_out_sums, d.lut_out_sums, ni * FR * sizeof(double), cudaMemcpyDeviceToHost));
-        CK(cudaMemcpy(hb->lut_out_counts, d.lut_out_counts, ni * FR * sizeof(int32_t), cudaMemcpyDeviceToHost));
+        CK(cudaMemcpyAsync(hb->lut_out_sums, d.lut_out_sums, ni * FR * sizeof(double), cudaMemcpyDeviceToHost, 0));
+        CK(cudaMemcpyAsync(hb->lut_out_counts, d.lut_out_counts, ni * FR * sizeof(int32_t), cudaMemcpyDeviceToHost, 0));
     }
+    CK(cudaStreamSynchronize(0));
+    if (elapsed_ms) cudaEventElapsedTime(elapsed_ms, e0, e1);
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
     return SLOSIM_OK;
 }
 
