@@ -1112,73 +1112,84 @@ __device__ __noinline__ bool quot_gt_exact(double a, double x, double b, double 
 // the occupied-lane set rk_mask) and reused when the slot set is unchanged and
 // every slot still compares above its rank predecessor: the old rank order is
 // then still sorted, so the ranks are unchanged.
-__device__ __forceinline__ int scan_geo(const LutMem* L, const Geo& g, uint32_t amask, int an, const Slot& sl,
-                                        int64_t vmin, uint32_t& adm, int& mseq, int& rk_rank, int& rk_pred,
-                                        uint32_t& rk_mask, int lane) {
+__device__ __forceinline__ int scan_geo(const LutMem* L, const Geo& g, const RowP* rowtab, uint32_t amask, int an,
+                                        const Slot& sl, int64_t vmin, uint32_t& adm, int& mseq, int& rk_rank,
+                                        int& rk_pred, uint32_t& rk_mask, int lane) {
     const bool occ = (amask >> lane) & 1u;
     const uint64_t key = occ ? (((uint64_t)(uint32_t)sl.seq << 32) | (uint32_t)sl.idr) : ~0ULL;
     int rank = rk_rank, pred = rk_pred;
     const uint64_t kp = __shfl_sync(FULLMASK, key, pred);
     if (rk_mask != amask || __any_sync(FULLMASK, occ && rank > 0 && !(kp < key))) {
-    rank = 0;
-    pred = lane;
-    uint64_t best = 0;
-    for (uint32_t m = amask; m;) {
-        const int j1 = __ffs((int)m) - 1;
-        m &= m - 1;
-        const int j2 = m ? __ffs((int)m) - 1 : j1;
-        m &= m - 1;
-        const uint64_t k1 = __shfl_sync(FULLMASK, key, j1), k2 = __shfl_sync(FULLMASK, key, j2);
-        const bool l1 = k1 < key, l2 = k2 < key && j2 != j1;
-        rank += (int)l1 + (int)l2;
-        if (l1 && k1 >= best) { best = k1; pred = j1; }
-        if (l2 && k2 >= best) { best = k2; pred = j2; }
-    }
-    rk_rank = rank;
-    rk_pred = pred;
-    rk_mask = amask;
+        rank = 0;
+        pred = lane;
+        uint64_t best = 0;
+        for (uint32_t m = amask; m;) {
+            const int j1 = __ffs((int)m) - 1;
+            m &= m - 1;
+            const int j2 = m ? __ffs((int)m) - 1 : j1;
+            m &= m - 1;
+            const uint64_t k1 = __shfl_sync(FULLMASK, key, j1), k2 = __shfl_sync(FULLMASK, key, j2);
+            const bool l1 = k1 < key, l2 = k2 < key && j2 != j1;
+            rank += (int)l1 + (int)l2;
+            if (l1 && k1 >= best) { best = k1; pred = j1; }
+            if (l2 && k2 >= best) { best = k2; pred = j2; }
+        }
+        rk_rank = rank;
+        rk_pred = pred;
+        rk_mask = amask;
     }
     const ColSel cs = gcol(g, occ ? sl.seq : 1);
     int b = 0, s = 0;
     double tcur = 0.0;
     adm = 0;
     mseq = 0;
-    double x = geval(L, g, grows(g, rank + 1), cs);
+    double x = geval_p(L, g, rowtab[occ ? rank + 1 : 1], cs);
     const int llast = __ffs((int)__ballot_sync(FULLMASK, occ && rank == an - 1)) - 1;
     const double smin = xsub((double)vmin, __shfl_sync(FULLMASK, x, llast));
     bool first = true;
     for (;;) {
         const bool valid = occ && rank >= s;
         const int bx = b + (rank - s) + 1;
-        if (!first) x = geval(L, g, grows(g, bx), cs);
+        if (!first) x = geval_p(L, g, rowtab[valid ? bx : 1], cs);
         first = false;
-        const double y = geval(L, g, grows(g, b + 1), cs);
         const double xprev = __shfl_sync(FULLMASK, x, pred);
         const double tprev = rank == s ? tcur : xprev;
         const int bprev = bx - 1;
-        bool tx, ty;
+        bool tx;
         bool qx = quot_gt_fast((double)(bprev + 1), x, (double)bprev, tprev, tx);
-        bool qy = quot_gt_fast((double)(b + 1), y, (double)b, tcur, ty);
-        const bool vy = occ && rank > s;
         const bool ex = valid && x <= smin && bprev != 0 && tx;
-        const bool ey = vy && y <= smin && b != 0 && ty;
-        if (__any_sync(FULLMASK, ex || ey)) {
+        if (__any_sync(FULLMASK, ex))
             if (ex) qx = quot_gt_exact((double)(bprev + 1), x, (double)bprev, tprev);
-            if (ey) qy = quot_gt_exact((double)(b + 1), y, (double)b, tcur);
-        }
         const bool okx = valid && x <= smin && (bprev == 0 || qx);
-        const bool oky = vy && y <= smin && (b == 0 || qy);
         const int f = __reduce_min_sync(FULLMASK, (valid && !okx) ? rank : an);
-        const int gy = __reduce_min_sync(FULLMASK, oky ? rank : an);
-        const bool run = f > s;
-        if (!run && gy >= an) break;  // Y admits nothing: the window is rejected
-        const int last = run ? f - 1 : gy;
+        int last, cnt;
+        double tsel;
+        if (f > s) {  // X: ranks [s, f) admitted, rank f rejected under the new state
+            last = f - 1;
+            cnt = f - s;
+            tsel = x;
+            adm |= __ballot_sync(FULLMASK, valid && rank < f);
+        } else {      // Y: rank s rejected; the lowest rank admissible under the unchanged state
+            const bool vy = occ && rank > s;
+            const double y = geval_p(L, g, rowtab[b + 1], cs);
+            bool ty;
+            bool qy = quot_gt_fast((double)(b + 1), y, (double)b, tcur, ty);
+            const bool ey = vy && y <= smin && b != 0 && ty;
+            if (__any_sync(FULLMASK, ey))
+                if (ey) qy = quot_gt_exact((double)(b + 1), y, (double)b, tcur);
+            const bool oky = vy && y <= smin && (b == 0 || qy);
+            const int gy = __reduce_min_sync(FULLMASK, oky ? rank : an);
+            if (gy >= an) break;  // the window is rejected
+            last = gy;
+            cnt = 1;
+            tsel = y;
+            adm |= __ballot_sync(FULLMASK, occ && rank == gy);
+        }
         const int ll = __ffs((int)__ballot_sync(FULLMASK, occ && rank == last)) - 1;
-        adm |= __ballot_sync(FULLMASK, occ && (run ? (rank >= s && rank < f) : rank == gy));
-        tcur = __shfl_sync(FULLMASK, run ? x : y, ll);
+        tcur = __shfl_sync(FULLMASK, tsel, ll);
         mseq = __shfl_sync(FULLMASK, sl.seq, ll);
-        b += run ? f - s : 1;
-        s = last + (run ? 2 : 1);  // X: rank f is rejected under the new state
+        s = f > s ? f + 1 : last + 1;
+        b += cnt;
         if (s >= an) break;
     }
     return b;
@@ -1375,6 +1386,14 @@ __device__ SIM_INLINE void simulate(const Ctx& cx, int64_t ii, const WS& w, int 
     int rk_rank = 0, rk_pred = lane;  // cached slot ranks of the kairos scan (scan_geo)
     uint32_t rk_mask = 0;
     const Geo geo = G ? geo_of(ST) : Geo{0, 0, 0};
+    // row selections of batch sizes 1..32 for the register-mode scan (per warp)
+    __shared__ RowP row_tabs[4][33];
+    RowP* const rowtab = row_tabs[threadIdx.x >> 5];
+    if (G) {
+        rowtab[lane + 1] = rowp_of(geo, lane + 1);
+        if (lane == 0) rowtab[0] = rowp_of(geo, 1);
+        __syncwarp();
+    }
     S.est_tok = S.P->est_tokens;
     S.est_busy = S.P->est_busy_us;
     S.rng = Pcg64{I->rng_state_hi, I->rng_state_lo, I->rng_inc_hi, I->rng_inc_lo};
@@ -1542,8 +1561,8 @@ __device__ SIM_INLINE void simulate(const Ctx& cx, int64_t ii, const WS& w, int 
                     int b;
                     if (G && __builtin_expect(lut_full, 1)) {
                         int msq;
-                        b = scan_geo(L, geo, amask, an, sl, wmin64_redux(v), adm, msq, rk_rank, rk_pred, rk_mask,
-                                     lane);
+                        b = scan_geo(L, geo, rowtab, amask, an, sl, wmin64_redux(v), adm, msq, rk_rank, rk_pred,
+                                     rk_mask, lane);
                         ms = msq;
                     } else if (__builtin_expect(lut_full, 1)) {
                         b = scan_slots<G>(L, amask, an, sl, wmin64_redux(v), adm, ms, lane);

@@ -292,6 +292,22 @@ __device__ __forceinline__ double geval(const LutMem* L, const Geo& g, const Row
     return rs.r2 < 0 ? v1 : r;
 }
 
+// Row selection of batch sizes 1..32 (the register-mode scan) as a per-warp
+// table: rows r1, r2 (r2 = r1 for a single row) and the Python-form weight
+// num * 2^-lo.  A single row then evaluates as v1 + (v1 - v1) * 0 = v1 exactly
+// (LUT means are positive), so the evaluation needs no select.
+struct RowP { int16_t r1, r2; int32_t num; double inv; };
+__device__ __forceinline__ RowP rowp_of(const Geo& g, int bsz) {
+    const RowSel rs = grows(g, bsz);
+    return RowP{(int16_t)rs.r1, (int16_t)(rs.r2 < 0 ? rs.r1 : rs.r2), (int32_t)rs.num, rs.inv};
+}
+__device__ __forceinline__ double geval_p(const LutMem* L, const Geo& g, const RowP& rp, const ColSel& cs) {
+    const int k1 = rp.r1 * g.ns + cs.c, k2 = rp.r2 * g.ns + cs.c;
+    const double v1 = xadd(xmul(L->slope[k1], cs.dx), L->mean[k1]);
+    const double v2 = xadd(xmul(L->slope[k2], cs.dx), L->mean[k2]);
+    return xadd(v1, xmul(xmul(xsub(v2, v1), (double)rp.num), rp.inv));
+}
+
 __device__ __forceinline__ void st_if(bool p, double* a, double v) {
     asm volatile("{\n\t.reg .pred q;\n\tsetp.ne.u32 q, %0, 0;\n\t@q st.f64 [%1], %2;\n\t}" ::"r"((unsigned)p), "l"(a),
                  "d"(v) : "memory");
