@@ -214,6 +214,9 @@ def main():
     if os.environ.get("GOLDEN_ONLY") == "extra":
         make_extra_golden(slosim)
         return
+    if os.environ.get("GOLDEN_ONLY") == "geo":
+        make_geo_golden(slosim)
+        return
 
     out = {"meta": {"reference": "slosim @ /root/reference/pkg/src", "numpy": __import__("numpy").__version__}}
     # --- config 1: 6 rates x 2 pairs on gen_longtail(LongTailSpec())
@@ -244,6 +247,68 @@ def main():
     make_event_golden(slosim)
     make_policy_golden(slosim)
     make_extra_golden(slosim)
+    make_geo_golden(slosim)
+
+
+def make_geo_golden(slosim):
+    """Engine cases for the power-of-two LUT geometry path with arbitrary LUT values:
+    fully populated file-backed profiles on bsz buckets 2^0..2^(nb-1) and seq buckets
+    (j+1)*2^w (index arithmetic, exact power-of-two divisions) with fractional
+    entries, frozen ground truth, noise, slack-guided and continuous decode, and
+    synthesized profiles on reduced power-of-two grids (fast-forward paths)."""
+    import tempfile
+
+    rng = random.Random(4242)
+    cases = []
+    tmp = tempfile.mkdtemp()
+    for k in range(40):
+        burst = rng.random() < 0.5
+        n = rng.randrange(40, 120) if burst else rng.randrange(20, 90)
+        wl = []
+        for i in range(n):
+            inp = rng.choice([rng.randrange(1, 900), rng.randrange(1, 5000), rng.randrange(20000, 70000)])
+            arr = rng.randrange(0, 60_000) if burst else rng.randrange(0, 4_000_000)
+            wl.append(slosim.Request(id=f"g{i:03d}", arrival_time=arr, input_len=inp,
+                                     output_len=rng.choice([1, rng.randrange(2, 80), rng.randrange(50, 300)]),
+                                     prefix_hit_len=rng.randrange(0, inp) if rng.random() < 0.1 else 0))
+        wl.sort(key=lambda r: r.arrival_time)
+        nb = rng.randrange(2, 10)
+        w = rng.choice([10, 12, 13, 14])
+        ns = rng.randrange(2, min(64, (160_000 >> w) + 2))
+        bszs = [1 << i for i in range(nb)]
+        seqs = [(j + 1) << w for j in range(ns)]
+        profile_json = None
+        if k % 2 == 0:
+            entries = [[float(rng.randrange(3_000, 60_000)) + rng.choice([0.0, 0.25, 0.5, 0.125]) for _ in seqs]
+                       for _ in bszs]
+            counts = [[rng.randrange(1, 50) for _ in seqs] for _ in bszs]
+            profile_json = {"bsz_buckets": bszs, "seq_buckets": seqs, "entries_us": entries, "counts": counts,
+                            "prefill_anchor": {"tokens": rng.choice([10_000, 131072]),
+                                               "duration_us": rng.choice([1_000_000, 8_800_000])}}
+            path = os.path.join(tmp, f"g{k}.json")
+            with open(path, "w") as f:
+                json.dump(profile_json, f)
+            prof = slosim.CostProfile(profile_path=path, decode_noise_eps=rng.choice([0.0, 0.2]))
+        else:
+            prof = slosim.CostProfile(bsz_buckets=bszs, seq_buckets=seqs, decode_noise_eps=rng.choice([0.0, 0.0, 0.2]),
+                                      prior_weight=rng.choice([1, 100]))
+        pp = ["fcfs", "sjf", "kairos-urgency"][k % 3]
+        dp = ["kairos-slack", "continuous", "kairos-slack"][(k // 3) % 3]
+        cfg = slosim.ClusterConfig(prefill_policy=pp, decode_policy=dp, profile=prof, seed=rng.randrange(100),
+                                   kv_capacity_tokens=rng.choice([2_000_000, 400_000]),
+                                   chunk_budget=rng.choice([8192, 2048]),
+                                   slo=slosim.SLOConfig(tpot_slo_us=rng.choice([50_000, 150_000, 400_000])))
+        try:
+            s = run_reference(slosim, cfg, wl)
+        except slosim.ConfigurationError:
+            continue
+        cj = cfg_to_json(cfg)
+        cj["profile"]["profile_json"] = profile_json
+        cases.append({"workload": wl_to_json(wl), "config": cj, "summary": s})
+    path = os.path.join(HERE, "geo_golden.json.gz")
+    with gzip.open(path, "wt", encoding="utf-8") as f:
+        json.dump(cases, f, sort_keys=True)
+    print("wrote", path, len(cases), os.path.getsize(path))
 
 
 def make_extra_golden(slosim):

@@ -79,6 +79,27 @@ def test_sparse_profiles_and_wide_active_sets_match_reference_golden(lib):
         assert summary_mismatches(got2[i], c["summary"]) == [], i
 
 
+def test_power_of_two_geometry_profiles_match_reference_golden(lib):
+    """The LUT geometry path (index arithmetic, exact power-of-two divisions, row table, fast-forward
+    with collapsed LUT updates) on full power-of-two grids with arbitrary (fractional) entries and on
+    reduced synthesized grids, through the row-recording and the throughput specialisations."""
+    from paper_2605_02329_b200 import _abi
+    from paper_2605_02329_b200.batch import run_batch
+
+    cases = load_golden("geo_golden.json.gz")
+    for flags in (_abi.F_ROWS, 0):
+        packed, _ = pack_cases(cases, flags=flags)
+        got = run_batch(packed)
+        bad = {}
+        for i, c in enumerate(cases):
+            m = summary_mismatches(got[i], c["summary"])
+            if flags and c["summary"]["status"] == 0:
+                m += row_mismatches(packed, i, c["summary"]["rows"])[:3]
+            if m:
+                bad[i] = m
+        assert not bad, f"flags={flags}: {len(bad)} cases differ: {dict(list(bad.items())[:5])}"
+
+
 def test_host_buffer_entry_point_matches(golden, lib):
     """slosim_run_batch_host (host buffers, copies inside) gives the same rows as the device path."""
     from paper_2605_02329_b200 import _abi

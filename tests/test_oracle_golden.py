@@ -85,6 +85,17 @@ def test_oracle_sparse_profiles_and_bursts_match_reference():
         assert row_mismatches(packed, i, c["summary"]["rows"]) == [], i
 
 
+def test_oracle_power_of_two_geometry_profiles_match_reference():
+    """Fully populated power-of-two LUT grids (file-backed with fractional entries, and synthesized)."""
+    cases = load_golden("geo_golden.json.gz")
+    packed, _ = pack_cases(cases, synth=oracle.synth)
+    oracle.run_batch(packed, threads=4)
+    for i, c in enumerate(cases):
+        assert summary_mismatches(packed.summaries[i], c["summary"]) == [], i
+        if c["summary"]["status"] == 0:
+            assert row_mismatches(packed, i, c["summary"]["rows"]) == [], i
+
+
 def test_oracle_event_logs_match_reference():
     """Full event logs, token timestamps, final LUT and estimator vs Simulation(collect_events=True)."""
     G = load_golden("events_golden.json.gz")
