@@ -172,7 +172,6 @@ __device__ __forceinline__ int decode_scan(const LutMem* L, int an, const int32_
     int b = 0;
     double tcur = 0.0;
     int64_t mseq = 0;
-    int nd = 0;
     if (L->full && an <= 32 && !audit_delayed) {
         // Dual-hypothesis rounds.  X: every candidate from s on is admitted, so
         // lane r tests with |B| = b + (r - s) and t_cur = x[r-1]; the first lane
