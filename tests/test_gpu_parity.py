@@ -130,3 +130,31 @@ def test_gpu_equals_oracle_on_config3_slice(lib):
             assert np.array_equal(a, b, equal_nan=True), k
         else:
             assert np.array_equal(a, b), k
+
+
+def _summaries_equal(got, want):
+    for k in [x for x in want.dtype.names if x != "sim_cycles"]:
+        a, b = got[k], want[k]
+        eq = np.array_equal(a, b, equal_nan=True) if a.dtype.kind == "f" else np.array_equal(a, b)
+        assert eq, k
+
+
+def test_gpu_equals_oracle_on_config2_and_config4_samples(lib):
+    """SURVEY Appendix B configs 2 (one 100k-request instance per pair) and 4 (5k-request
+    round-robin sub-traces): GPU vs oracle, all summary fields bit-exact."""
+    from oracle import oracle
+    from paper_2605_02329_b200.batch import config2, config4, run_batch
+
+    sw = config2()
+    got = run_batch(sw.packed).copy()
+    ref = config2(synth=oracle.synth)
+    oracle.run_batch(ref.packed, threads=2)
+    _summaries_equal(got, ref.packed.summaries)
+
+    kw = dict(seeds=range(3), n_requests=20_000)
+    sel = np.arange(0, 24, 5)
+    sw = config4(select=sel, **kw)
+    got = run_batch(sw.packed).copy()
+    ref = config4(select=sel, synth=oracle.synth, **kw)
+    oracle.run_batch(ref.packed, threads=8)
+    _summaries_equal(got, ref.packed.summaries)
