@@ -1542,6 +1542,7 @@ __device__ SIM_INLINE void simulate(const Ctx& cx, int64_t ii, const WS& w, int 
         // ---- start a decode step (engine.py:377-392): the hot path
         if (dc_end == SLOSIM_INF64 && an > 0) {
             PROF_COUNT(7, an == 1);
+            PROF_COUNT(6, an > 16 ? (an > 32 ? 1000000 : 1) : 0);
             v_dec += an;
             max_a = an > max_a ? an : max_a;
             int bsz = an;

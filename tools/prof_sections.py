@@ -35,5 +35,6 @@ for p in pairs:
     tot = v[:6].sum()
     print(f"{PAIRS_4[p]}: {tot / 1e9:.1f} Gcycles {tot / steps:.0f} cycles/decode-step, an==1 starts {v[7] / (s['v_dec'].sum() and steps):.2f} "
           f"of steps, ff calls {v[8]:.0f} ff steps {v[9]:.0f} ({v[9] / steps * 100:.1f}% of steps)")
+    print(f"   steps with 16 < an <= 32: {(v[6] % 1000000) / steps * 100:.2f}%, an > 32: {(v[6] // 1000000) / steps * 100:.2f}%")
     for k in range(6):
         print(f"   {NAMES[k]:22s} {v[k] / tot * 100:5.1f}%  {v[k] / steps:7.1f} cyc/step")
