@@ -82,13 +82,18 @@ def load_peaks():
 
 def profile_traffic(instances_per_launch):
     """DRAM bytes per launch of the dominant kernel from the committed `ncu --set full` capture
-    (profiles/ncu_summary.json), scaled per instance to this launch size; None if absent."""
+    (profiles/ncu_summary.json), scaled per instance to this launch size, plus the capture's
+    issue-slot and warp-efficiency counters; None if absent."""
     try:
         with open(os.path.join(ROOT, "profiles", "ncu_summary.json")) as f:
             d = json.load(f)
-        return d["dram_bytes_per_instance"] * instances_per_launch, d.get("capture")
+        m = d.get("metrics", {})
+        counters = {"smsp__issue_active_pct": float(m["smsp__issue_active.avg.pct_of_peak_sustained_active"]),
+                    "thread_inst_per_inst": float(m["smsp__thread_inst_executed_per_inst_executed.ratio"]),
+                    "no_instruction_stall_pct": d.get("stall_breakdown_pct", {}).get("no_instructions")}
+        return d["dram_bytes_per_instance"] * instances_per_launch, d.get("capture"), counters
     except Exception:
-        return None, None
+        return None, None, None
 
 
 class ClockSampler:
@@ -230,7 +235,9 @@ def main():
     n_total = N_CONFIG5 if args.workload == "config5" else (3072 if args.workload == "config3" else 2)
     slice_n = min(args.slice, n_total) if args.workload != "config2" else 2
     n_slices = max(1, n_total // slice_n)
+    t_pack = time.perf_counter()
     sw = build_workload(args.workload)
+    pack_s = time.perf_counter() - t_pack
     db = DeviceBatch(sw.packed)
     pk = sw.packed
     n_pairs, n_slo, n_rates = {"config5": (4, 16, 64), "config3": (3, 16, 64), "config2": (2, 1, 1)}[args.workload]
@@ -296,7 +303,9 @@ def main():
     abytes = alg_bytes(summ) / len(timed)
     mean_ms = float(np.mean(step_ms))
     achieved = abytes / (mean_ms / 1e3) / 1e9
-    traffic, traffic_src = profile_traffic(slice_n)
+    traffic, traffic_src, ncu_counters = profile_traffic(slice_n)
+    # compulsory floor of the byte model: the trace read (24 B/request) and the summary row (96 B/instance)
+    floor_bytes = 24 * reqs_rank / len(timed) + 96 * slice_n
 
     # e2e through the C-ABI with host buffers (pinned), copies inside the timed region
     e2e = None
@@ -319,7 +328,9 @@ def main():
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "peak_kind": peak_kind, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": traffic,
                          "traffic_source": f"ncu dram__bytes_read+write per instance x {slice_n} ({traffic_src})",
-                         "alg_bytes_per_launch": abytes, "mean_launch_ms": mean_ms},
+                         "alg_bytes_per_launch": abytes, "mean_launch_ms": mean_ms,
+                         "floor_bytes_per_launch": floor_bytes, "ncu_counters": ncu_counters},
+            "host_pack_s": round(pack_s, 2),
             "cpu_baseline": cpu,
             "parity": parity,
             "clocks": clocks,
