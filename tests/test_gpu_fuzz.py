@@ -2,8 +2,9 @@
 
 Thousands of random instances over every policy pair and knob the engine
 specialises on: default and custom bucket grids (the power-of-two geometry path
-and the table path), prior weights, noise, transfer delays, prefix hits, KV
-limits that gate admission, bursts beyond 32 concurrent decodes (memory mode),
+and the table path), one- to four-anchor decode curves (staged line or general
+formula), prefill ground-truth curves, prior weights, noise, transfer delays,
+prefix hits, KV limits that gate admission, bursts beyond 32 concurrent decodes (memory mode),
 long quiet stretches (fast-forward) and equal arrival times.  Every summary
 field and every per-request row must be bit-identical to the C oracle, through
 both the throughput and the row-recording specialisations.
@@ -52,8 +53,16 @@ def _config(rng, wl, k):
     elif grid == "table":
         bsz = sorted(rng.sample(range(1, 300), rng.randrange(2, 9)))
         seq = sorted(rng.sample(range(500, 200_000), rng.randrange(2, 20)))
-    prof = CostProfile(bsz_buckets=bsz, seq_buckets=seq, prior_weight=rng.choice([100, 100, 1, 7]),
-                       batch_growth=rng.choice([0.0, 0.03, 0.05]), decode_noise_eps=rng.choice([0.0, 0.0, 0.0, 0.2]))
+    anchors = rng.choice([
+        [(1, 8192, 11_000), (1, 131072, 40_300)],
+        [(1, 16384, 12_500)],
+        [(1, 1024, 9_000), (1, 65536, 42_000)],
+        [(1, 4096, 7_000), (1, 32768, 15_000), (1, 131072, 60_000), (4, 8192, 30_000)],
+    ])
+    curve = rng.choice([None, None, [(8192, 400_400), (131072, 8_800_000)], [(5000, 300_000), (50000, 4_000_000)]])
+    prof = CostProfile(decode_anchors=anchors, bsz_buckets=bsz, seq_buckets=seq,
+                       prior_weight=rng.choice([100, 100, 1, 7]), batch_growth=rng.choice([0.0, 0.03, 0.05]),
+                       prefill_gt_curve=curve, decode_noise_eps=rng.choice([0.0, 0.0, 0.0, 0.2]))
     worst = max(r.input_len + r.output_len for r in wl)
     return ClusterConfig(prefill_policy=pp, decode_policy=dp, profile=prof, seed=rng.randrange(1000),
                          kv_capacity_tokens=worst + rng.choice([0, rng.randrange(0, 200_000), 2_000_000]),
