@@ -6,7 +6,12 @@
 // holds the same scalar state (time, pool status, counters) and the lanes
 // cooperate on the per-request sets (prefill queue, pending admission list,
 // active decode set), which live in a per-warp SoA workspace that stays
-// L1-resident for the life of an instance.
+// L1-resident for the life of an instance; up to 32 active decode requests
+// live in the lanes' registers (Slot).  Decode steps between rare events are
+// applied in bulk where the batch cannot change (ff_steps), and the LUT has a
+// power-of-two geometry path (lut.cuh).  The kernel is instruction-fetch
+// bound, so the hot loop is kept short and every rare event runs out of line
+// (DESIGN.md §5).
 //
 // Reference mapping (engine.py):
 //   instant loop :264-271                      -> simulate() main loop
@@ -1331,8 +1336,8 @@ __device__ __noinline__ int ff_steps(Sim& S, Slot& sl, int64_t t, int lane) {
 #endif
 
 // DP: decode policy (compile-time), FULL: event trace / per-request rows / LUT
-// export compiled in.  The throughput path runs simulate<DP, false>, whose hot
-// loop carries no tracing or row-output code.
+// export compiled in, G: power-of-two LUT geometry.  The throughput path runs
+// simulate<DP, false, G>, whose hot loop carries no tracing or row-output code.
 #ifdef SLOSIM_SIM_NOINLINE
 #define SIM_INLINE __noinline__
 #else
