@@ -258,6 +258,9 @@ int slosim_abi_version(void);
 int slosim_device_count(void);
 const char* slosim_build_info(void);
 
+/* Text of the last CUDA error of this thread (valid after a SLOSIM_ECUDA return). */
+const char* slosim_last_error(void);
+
 #ifdef __cplusplus
 }
 #endif

@@ -236,6 +236,7 @@ def lib():
 
 # exported C symbols that include/slosim_b200.h declares (checked by tests)
 HEADER_SYMBOLS = [
+    "slosim_last_error",
     "slosim_run_batch",
     "slosim_run_batch_host",
     "slosim_workspace_bytes",
