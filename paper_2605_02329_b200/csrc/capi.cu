@@ -234,16 +234,20 @@ extern "C" int slosim_run_batch_host(const slosim_batch_t* hb, float* elapsed_ms
     CK(up((slosim_instance_t*)d.instances, hb->instances, ni));
     CK(up((int64_t*)d.order, order.data(), ni));
     if (!hb->trace_buf) d.trace_buf = nullptr;
-    cudaEvent_t e0, e1;
-    CK(cudaEventCreate(&e0));
-    CK(cudaEventCreate(&e1));
-    CK(cudaEventRecord(e0, 0));
+    struct Events {  // destroyed on every return path
+        cudaEvent_t e0 = nullptr, e1 = nullptr;
+        ~Events() {
+            if (e0) cudaEventDestroy(e0);
+            if (e1) cudaEventDestroy(e1);
+        }
+    } ev;
+    CK(cudaEventCreate(&ev.e0));
+    CK(cudaEventCreate(&ev.e1));
+    CK(cudaEventRecord(ev.e0, 0));
     int rc = slosim_run_batch(&d, nullptr);
-    CK(cudaEventRecord(e1, 0));
+    CK(cudaEventRecord(ev.e1, 0));
     if (rc) {
-        cudaEventSynchronize(e1);
-        cudaEventDestroy(e0);
-        cudaEventDestroy(e1);
+        cudaEventSynchronize(ev.e1);
         return rc;
     }
     CK(cudaMemcpyAsync(hb->summaries, d.summaries, ni * sizeof(slosim_summary_t), cudaMemcpyDeviceToHost, 0));
@@ -262,9 +266,7 @@ extern "C" int slosim_run_batch_host(const slosim_batch_t* hb, float* elapsed_ms
         CK(cudaMemcpyAsync(hb->lut_out_counts, d.lut_out_counts, ni * FR * sizeof(int32_t), cudaMemcpyDeviceToHost, 0));
     }
     CK(cudaStreamSynchronize(0));
-    if (elapsed_ms) cudaEventElapsedTime(elapsed_ms, e0, e1);
-    cudaEventDestroy(e0);
-    cudaEventDestroy(e1);
+    if (elapsed_ms) cudaEventElapsedTime(elapsed_ms, ev.e0, ev.e1);
     return SLOSIM_OK;
 }
 
