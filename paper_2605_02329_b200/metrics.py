@@ -16,7 +16,7 @@ from dataclasses import dataclass, field
 import numpy as np
 
 from . import _abi
-from .domain import Request, SLOConfig, SimTime
+from .domain import Request, SLOConfig
 
 
 @dataclass

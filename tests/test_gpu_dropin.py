@@ -8,8 +8,6 @@
   restated as fresh tests against this package.
 """
 
-import copy
-import math
 
 import numpy as np
 import pytest

@@ -1,12 +1,11 @@
 """CPU: host-side input packing (traces, rescale, sweep grids, histogram cells)."""
 
 import numpy as np
-import pytest
 
 from paper_2605_02329_b200 import dist as D
-from paper_2605_02329_b200.batch import PAIRS_4, SWEEP_RATES, SWEEP_SLO_SCALES, config3, grid_batch
+from paper_2605_02329_b200.batch import SWEEP_RATES, SWEEP_SLO_SCALES, config3
 from paper_2605_02329_b200.domain import Request
-from paper_2605_02329_b200.workload import (LongTailSpec, gen_longtail, longtail_arrays, rescale_factor, rescale_qps,
+from paper_2605_02329_b200.workload import (LongTailSpec, longtail_arrays, rescale_factor, rescale_qps,
                                             trace_arrays_from_requests)
 
 
