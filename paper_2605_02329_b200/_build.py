@@ -44,8 +44,8 @@ def build(force: bool = False, verbose: bool = False) -> str:
     os.replace(OUT + ".tmp", OUT)
     if verbose:
         print(r.stderr)
-    with open(os.path.join(CSRC, "ptxas_info.txt"), "w") as f:
-        f.write(r.stderr)
+    with open(os.path.join(CSRC, "ptxas_info.txt"), "w") as f:  # register/spill report (no timings: stable diffs)
+        f.write("".join(l for l in r.stderr.splitlines(True) if "Compile time" not in l))
     return OUT
 
 
