@@ -47,6 +47,10 @@ struct Arena {
         size_t want = std::max(bytes, (size_t)1 << 20);
         cudaError_t e = cudaMalloc(&ptr, want);
         if (e != cudaSuccess) { ptr = nullptr; return e; }
+        // zero once per allocation: the engine's branch-free LUT update reads (and discards) the
+        // neighbour of an edge cell, which may lie outside the live part of a workspace LUT
+        e = cudaMemset(ptr, 0, want);
+        if (e != cudaSuccess) return e;
         size = want;
         device = dev;
         return cudaSuccess;
