@@ -253,6 +253,16 @@ int slosim_request_metrics(int64_t n, const double* arrival, const int64_t* outp
 int slosim_histogram(int64_t n, const slosim_summary_t* d_summaries, const int32_t* d_cell, int32_t n_bins,
                      int64_t* d_hist, void* stream);
 
+/* Replaces the final merge of a sharded sweep (the C-ABI form of
+ * paper_2605_02329_b200.dist.exchange): over the caller's NCCL communicator
+ * (`nccl_comm` is an ncclComm_t), sum-all-reduce the int64 histogram d_hist[n_hist]
+ * in place and all-gather n_mine summary rows per rank from d_mine into d_all
+ * (rank order, n_mine * world rows).  DEVICE pointers, stream-ordered; integer sums
+ * make the result independent of the rank count.  NCCL (libnccl.so.2) is resolved
+ * at run time; returns SLOSIM_ECUDA with slosim_last_error() if it is missing. */
+int slosim_exchange(void* nccl_comm, const slosim_summary_t* d_mine, int64_t n_mine, slosim_summary_t* d_all,
+                    int64_t* d_hist, int64_t n_hist, void* stream);
+
 /* Library identity (ABI version, sm arch compiled for) and visible CUDA devices. */
 int slosim_abi_version(void);
 int slosim_device_count(void);

@@ -224,6 +224,7 @@ def lib():
     L.slosim_prefill_batch_us.argtypes = [c_int32, vp, vp, c_int32, vp, vp, vp]
     L.slosim_request_metrics.argtypes = [c_int64, vp, vp, vp, vp, c_int64, c_int64, vp, vp, vp, vp, vp, vp]
     L.slosim_histogram.argtypes = [c_int64, vp, vp, c_int32, vp, vp]
+    L.slosim_exchange.argtypes = [vp, vp, c_int64, vp, vp, c_int64, vp]
     L.slosim_abi_version.restype = c_int
     L.slosim_last_error.restype = c_char_p
     L.slosim_build_info.restype = c_char_p
@@ -237,6 +238,7 @@ def lib():
 # exported C symbols that include/slosim_b200.h declares (checked by tests)
 HEADER_SYMBOLS = [
     "slosim_last_error",
+    "slosim_exchange",
     "slosim_run_batch",
     "slosim_run_batch_host",
     "slosim_workspace_bytes",

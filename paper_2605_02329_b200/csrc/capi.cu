@@ -3,6 +3,7 @@
 // policies and cost models of the engine one decision at a time.  The snapshot
 // kernels call the very same device functions as the batched engine.
 #include <cuda_runtime.h>
+#include <dlfcn.h>
 #include <math.h>
 #include <stdio.h>
 #include <stdlib.h>
@@ -837,6 +838,58 @@ extern "C" const char* slosim_build_info(void) {
 }
 
 extern "C" const char* slosim_last_error(void) { return g_err; }
+
+// ---------------------------------------------------------------- exchange --
+namespace {
+// NCCL entry points resolved at run time (no link-time dependency; an already
+// loaded libnccl.so.2, e.g. PyTorch's, is reused).  Enum values per nccl.h.
+typedef int (*nccl_allreduce_fn)(const void*, void*, size_t, int, int, void*, cudaStream_t);
+typedef int (*nccl_allgather_fn)(const void*, void*, size_t, int, void*, cudaStream_t);
+typedef const char* (*nccl_errstr_fn)(int);
+constexpr int kNcclUint8 = 1, kNcclInt64 = 4, kNcclSum = 0;
+struct Nccl {
+    nccl_allreduce_fn all_reduce = nullptr;
+    nccl_allgather_fn all_gather = nullptr;
+    nccl_errstr_fn err = nullptr;
+    bool tried = false;
+};
+Nccl& nccl() {
+    static Nccl n;
+    std::lock_guard<std::mutex> lock(g_mu);
+    if (!n.tried) {
+        n.tried = true;
+        void* h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_NOLOAD);
+        if (!h) h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_LOCAL);
+        if (h) {
+            n.all_reduce = (nccl_allreduce_fn)dlsym(h, "ncclAllReduce");
+            n.all_gather = (nccl_allgather_fn)dlsym(h, "ncclAllGather");
+            n.err = (nccl_errstr_fn)dlsym(h, "ncclGetErrorString");
+        }
+    }
+    return n;
+}
+}  // namespace
+
+extern "C" int slosim_exchange(void* nccl_comm, const slosim_summary_t* d_mine, int64_t n_mine, slosim_summary_t* d_all,
+                               int64_t* d_hist, int64_t n_hist, void* stream) {
+    if (!nccl_comm || n_mine < 0 || n_hist < 0 || (n_mine && (!d_mine || !d_all)) || (n_hist && !d_hist))
+        return SLOSIM_EINVAL;
+    Nccl& n = nccl();
+    if (!n.all_reduce || !n.all_gather) {
+        snprintf(g_err, sizeof(g_err), "slosim_exchange: libnccl.so.2 not loadable");
+        return SLOSIM_ECUDA;
+    }
+    cudaStream_t st = (cudaStream_t)stream;
+    int r = 0;
+    if (n_hist) r = n.all_reduce(d_hist, d_hist, (size_t)n_hist, kNcclInt64, kNcclSum, nccl_comm, st);
+    if (!r && n_mine)
+        r = n.all_gather(d_mine, d_all, (size_t)n_mine * sizeof(slosim_summary_t), kNcclUint8, nccl_comm, st);
+    if (r) {
+        snprintf(g_err, sizeof(g_err), "slosim_exchange: NCCL error %d (%s)", r, n.err ? n.err(r) : "?");
+        return SLOSIM_ECUDA;
+    }
+    return SLOSIM_OK;
+}
 
 #ifdef SLOSIM_PROF
 // Debug builds only: read (and optionally reset) the section-profile counters of the engine loop.
