@@ -8,7 +8,7 @@ import subprocess
 HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 OUT = os.path.join(HERE, "libslosim_b200.so")
-SOURCES = ["capi.cu"]
+SOURCES = ["capi.cu", "engine_lat.cu"]
 HEADERS = ["engine.cuh", "lut.cuh", "numerics.cuh", os.path.join("..", "..", "include", "slosim_b200.h")]
 
 NVCC_FLAGS = [

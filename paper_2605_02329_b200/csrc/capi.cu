@@ -17,6 +17,10 @@
 
 using namespace slosim;
 
+// engine_lat.cu: the engine built for one block per SM (no spills), for small batches
+cudaError_t slosim_launch_latency_engine(int grid, const void* cx, char* ws, size_t stride, int64_t cap,
+                                         unsigned long long* work, cudaStream_t st);
+
 namespace {
 
 thread_local char g_err[512];
@@ -128,8 +132,13 @@ extern "C" int slosim_run_batch(const slosim_batch_t* b, void* stream) {
     cx.B = *b;
     cx.sched_tab = sched;
     cx.frozen_tab = frozen;
-    sim_kernel<<<grid, 128, 0, st>>>(cx, (char*)g_ws.ptr, stride, cap, (unsigned long long*)g_work.ptr);
-    CK(cudaGetLastError());
+    if (b->n_instances <= (int64_t)g_sms * 4 && !getenv("SLOSIM_NO_LATENCY_ENGINE")) {
+        // at most one 4-warp block per SM: the spill-free latency build (engine_lat.cu)
+        CK(slosim_launch_latency_engine(grid, &cx, (char*)g_ws.ptr, stride, cap, (unsigned long long*)g_work.ptr, st));
+    } else {
+        sim_kernel<<<grid, 128, 0, st>>>(cx, (char*)g_ws.ptr, stride, cap, (unsigned long long*)g_work.ptr);
+        CK(cudaGetLastError());
+    }
     return SLOSIM_OK;
 }
 

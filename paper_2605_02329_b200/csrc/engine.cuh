@@ -93,6 +93,7 @@ __device__ __forceinline__ WS make_ws(char* base, int64_t cap) {
 }
 
 // Per-profile LUT tables (scheduler seed + frozen ground truth), built once per launch.
+#ifndef SLOSIM_ENGINE_ONLY
 __global__ void build_profile_tables(const slosim_profile_t* profiles, int n_profiles, LutMem* sched,
                                      LutMem* frozen) {
     int lane = threadIdx.x & 31;
@@ -102,6 +103,7 @@ __global__ void build_profile_tables(const slosim_profile_t* profiles, int n_pro
     lut_build(sched + p, P->nb, P->ns, P->bsz_buckets, P->seq_buckets, P->lut_sums, P->lut_counts, lane);
     lut_build(frozen + p, P->nb, P->ns, P->bsz_buckets, P->seq_buckets, P->gt_sums, P->gt_counts, lane);
 }
+#endif
 
 // ------------------------------------------------------------ trace writer --
 struct TraceW {
