@@ -132,7 +132,8 @@ extern "C" int slosim_run_batch(const slosim_batch_t* b, void* stream) {
     cx.B = *b;
     cx.sched_tab = sched;
     cx.frozen_tab = frozen;
-    if (b->n_instances <= (int64_t)g_sms * 4 && !getenv("SLOSIM_NO_LATENCY_ENGINE")) {
+    const bool force_lat = getenv("SLOSIM_FORCE_LATENCY_ENGINE") != nullptr;  // experiment knob
+    if ((b->n_instances <= (int64_t)g_sms * 4 || force_lat) && !getenv("SLOSIM_NO_LATENCY_ENGINE")) {
         // at most one 4-warp block per SM: the spill-free latency build (engine_lat.cu)
         CK(slosim_launch_latency_engine(grid, &cx, (char*)g_ws.ptr, stride, cap, (unsigned long long*)g_work.ptr, st));
     } else {
