@@ -10,22 +10,34 @@ a 256 MiB write) followed by the final exchange: the per-(pair, rate, SLO)
 e2e-attainment histogram build, an NCCL int64 all-reduce and an all-gather of
 the summary rows.
 
+`--gpus N` runs N ranks, one per GPU: launched under torchrun (WORLD_SIZE set)
+it checks WORLD_SIZE == N; launched plainly with N > 1 it re-executes itself
+under `torch.distributed.run` with N local ranks.  A mismatch, or fewer
+visible GPUs than N, exits non-zero instead of measuring fewer GPUs.
+SLOSIM_DIST_BACKEND=gloo lets N ranks share one GPU (tests only).
+
 JSON line keys follow the driver contract; `e2e` re-measures the same metric
 through the C-ABI host-buffer entry point (slosim_run_batch_host) with pinned
 host inputs and every H2D/D2H copy inside the timed region; `roofline` uses
 the SURVEY §8(d) algorithmic byte model; `cpu_baseline` times the C oracle
 port (all host threads) on a bounded sample of the same slice and checks the
-GPU results against it bit-for-bit.
+GPU results against it bit-for-bit; `cpu_baseline_python` times the
+unmodified Python reference (baseline/_ref, when installed) on a stride
+sample through its own `slosim.run`, and checks the GPU results against it.
 
-    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl reference] [--workload config5|config3|config2]
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl reference]
+                    [--workload config5|config4|config3|config2|config1]
 """
 
 from __future__ import annotations
 
 import argparse
 import ctypes
+import hashlib
 import json
 import os
+import platform
+import socket
 import subprocess
 import sys
 import tempfile
@@ -37,21 +49,29 @@ ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
 SLICE = 16384
-N_CONFIG5 = 256 * 64 * 16 * 4
+# instances of each SURVEY Appendix B config and its (pairs, SLO scales, rates) histogram grid
+N_TOTAL = {"config1": 12, "config2": 2, "config3": 3072, "config4": 2048, "config5": 256 * 64 * 16 * 4}
+GRID = {"config1": (2, 1, 6), "config2": (2, 1, 1), "config3": (3, 16, 64), "config4": (2, 1, 1),
+        "config5": (4, 16, 64)}
+# reference-arm sample per step (bounded CPU work)
+REF_SAMPLE = {"config1": 12, "config2": 2, "config3": 768, "config4": 256, "config5": 1536}
+N_BINS = 1001
 
 
-def parse():
+def parse(argv=None):
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--workload", default="config5", choices=["config5", "config3", "config2"])
-    ap.add_argument("--slice", type=int, default=SLICE)
+    ap.add_argument("--workload", default="config5", choices=sorted(N_TOTAL))
+    ap.add_argument("--slice", type=int, default=SLICE, help="config5 instances per step per GPU")
     ap.add_argument("--cpu-sample-s", type=float, default=12.0, help="target seconds of oracle work")
+    ap.add_argument("--pyref-sample", type=int, default=-1,
+                    help="instances of the Python reference baseline (-1: workload default, 0: off)")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
-    return ap.parse_args()
+    return ap.parse_args(argv)
 
 
 def dist_env():
@@ -63,6 +83,10 @@ def dist_env():
 
 def metric_name():
     return "simulated requests/sec (1/2/4/8 B200) at oracle-exact SLO attainment vs CPU ref"
+
+
+def slice_size(args):
+    return min(args.slice, N_TOTAL[args.workload]) if args.workload == "config5" else N_TOTAL[args.workload]
 
 
 def alg_bytes(summ: np.ndarray) -> int:
@@ -80,7 +104,7 @@ def load_peaks():
         return 6650.0, "fallback"
 
 
-def profile_traffic(instances_per_launch):
+def profile_counters(instances_per_launch):
     """DRAM bytes per launch of the dominant kernel from the committed `ncu --set full` capture
     (profiles/ncu_summary.json), scaled per instance to this launch size, plus the capture's
     issue-slot and warp-efficiency counters; None if absent."""
@@ -90,10 +114,23 @@ def profile_traffic(instances_per_launch):
         m = d.get("metrics", {})
         counters = {"smsp__issue_active_pct": float(m["smsp__issue_active.avg.pct_of_peak_sustained_active"]),
                     "thread_inst_per_inst": float(m["smsp__thread_inst_executed_per_inst_executed.ratio"]),
-                    "no_instruction_stall_pct": d.get("stall_breakdown_pct", {}).get("no_instructions")}
+                    "no_instruction_stall_pct": d.get("stall_breakdown_pct", {}).get("no_instructions"),
+                    "warp_inst_per_request": d.get("warp_inst_per_request"),
+                    "instances_captured": d.get("instances")}
         return d["dram_bytes_per_instance"] * instances_per_launch, d.get("capture"), counters
     except Exception:
         return None, None, None
+
+
+def cpu_model():
+    try:
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                if line.startswith("model name"):
+                    return line.split(":", 1)[1].strip()
+    except Exception:
+        pass
+    return platform.processor() or "unknown"
 
 
 class ClockSampler:
@@ -145,26 +182,132 @@ class ClockSampler:
 def build_workload(name, synth=None, select=None):
     from paper_2605_02329_b200 import batch as B
 
-    if name == "config5":
-        return B.config5(select=select, synth=synth)
-    if name == "config3":
-        return B.config3(select=select, synth=synth)
-    return B.config2(select=select, synth=synth)
+    return B.CONFIGS[name](select=select, synth=synth)
 
 
 def workload_meta(name, slice_n):
+    l2 = "flushed between steps (256 MiB write)"
     if name == "config5":
         return {"workload": "config5: 256 seeds x 64 rates x 16 SLO scales x 4 policy pairs, 1k-request long-tail "
                             "traces (1,048,576 instances)", "instances_per_step_per_gpu": slice_n,
                 "requests_per_instance": 1000, "policy_pairs": ["fcfs+continuous", "fcfs+kairos-slack",
                                                                 "kairos-urgency+continuous",
-                                                                "kairos-urgency+kairos-slack"],
-                "l2": "flushed between steps (256 MiB write)"}
+                                                                "kairos-urgency+kairos-slack"], "l2": l2}
+    if name == "config4":
+        return {"workload": "config4: 256 seeds x 20k-request traces at qps 4.0, each split round-robin into 4 "
+                            "1P+1D pairs, x 2 policy pairs (2048 instances of 5k requests)", "l2": l2}
     if name == "config3":
         return {"workload": "config3: 64 rates x 16 SLO scales x 3 policy pairs on the config-1 trace (3072 instances)",
-                "l2": "flushed between steps (256 MiB write)"}
-    return {"workload": "config2: one 100k-request long-tail trace, kairos and fcfs pairs (2 instances)",
-            "l2": "flushed between steps (256 MiB write)"}
+                "l2": l2}
+    if name == "config1":
+        return {"workload": "config1: the default 1k-request trace x 6 CLI rates x 2 policy pairs (12 instances)",
+                "l2": l2}
+    return {"workload": "config2: one 100k-request long-tail trace, kairos and fcfs pairs (2 instances)", "l2": l2}
+
+
+# --------------------------------------------- Python reference (unmodified) --
+def _pyref_path():
+    p = os.path.join(ROOT, "baseline", "_ref")
+    return p if os.path.isdir(os.path.join(p, "slosim")) else None
+
+
+_PYREF_WL = {}
+
+
+def _pyref_init(path):
+    if path not in sys.path:
+        sys.path.insert(0, path)
+
+
+def _pyref_run(item):
+    """One instance through the reference's own public API: slosim.run(config, workload)."""
+    import slosim
+
+    key, pp, dp, ttft, tpot = item
+    wl = _PYREF_WL[key]
+    cfg = slosim.ClusterConfig(prefill_policy=pp, decode_policy=dp,
+                               slo=slosim.SLOConfig(ttft_slo_us=ttft, tpot_slo_us=tpot))
+    t0 = time.perf_counter()
+    rep = slosim.run(cfg, wl)
+    dt = time.perf_counter() - t0
+    n = len(rep.rows)
+    return {"n": n, "ttft_met": sum(r.ttft_met for r in rep.rows), "tpot_met": sum(r.tpot_met for r in rep.rows),
+            "e2e_met": sum(r.e2e_met for r in rep.rows), "p50": rep.decode_tps_p50, "p90": rep.decode_tps_p90,
+            "worst": rep.worst_queue_wait_us, "s": dt}
+
+
+def _pyref_workloads(name, sw, sel):
+    """Reference workloads (list[Request]) of the selected instances, built with the reference's own
+    generator and rescale; returns the per-instance work items."""
+    import slosim
+    from paper_2605_02329_b200 import batch as B
+
+    coords = sw.coords
+    items = []
+    for k, i in enumerate(sel):
+        c = coords[i]
+        pair = {"config1": B.PAIRS_2, "config2": B.PAIRS_2[::-1], "config3": B.PAIRS_3, "config4": B.PAIRS_2,
+                "config5": B.PAIRS_4}[name][int(c["pair"])]
+        scale = float(c["slo_scale"])
+        ttft, tpot = round(8_000_000 * scale), round(50_000 * scale)
+        if name in ("config1", "config3", "config5"):
+            seed = 2024 if name != "config5" else int(c["trace"])
+            key = (seed, float(c["rate"]))
+            if key not in _PYREF_WL:
+                _PYREF_WL[key] = slosim.rescale_qps(slosim.gen_longtail(slosim.LongTailSpec(seed=seed)), key[1])
+        elif name == "config2":
+            key = ("c2",)
+            if key not in _PYREF_WL:
+                _PYREF_WL[key] = slosim.gen_longtail(slosim.LongTailSpec(n_requests=100_000, seed=2024, qps=1.0))
+        else:  # config4: trace t = seed (t // 4), sub-trace j = t % 4 (split by position)
+            t = int(c["trace"])
+            key = ("c4", t)
+            if key not in _PYREF_WL:
+                full = slosim.gen_longtail(slosim.LongTailSpec(n_requests=20_000, seed=t // 4, qps=4.0))
+                _PYREF_WL[key] = full[t % 4::4]
+        items.append((key, pair[0], pair[1], ttft, tpot))
+    return items
+
+
+def python_reference_baseline(name, sw, got_summ, n_sample, threads):
+    """Time the unmodified reference (baseline/_ref) on a stride sample of the workload, all host cores
+    (one process per core, trace generation outside the timed region), and compare its reports with the
+    GPU summaries of the same instances."""
+    path = _pyref_path()
+    if path is None:
+        return {"unavailable": "baseline/_ref (the pip-installed reference) is not present"}
+    _pyref_init(path)
+    import multiprocessing as mp
+
+    n_total = len(got_summ)
+    n_sample = max(1, min(n_sample, n_total))
+    stride = n_total // n_sample
+    sel = np.arange(n_sample, dtype=np.int64) * stride + (stride // 2 if stride > 1 else 0)
+    items = _pyref_workloads(name, sw, sel)
+    ctx = mp.get_context("fork")
+    with ctx.Pool(min(threads, len(items)), initializer=_pyref_init, initargs=(path,)) as pool:
+        pool.map(abs, range(threads))  # workers up before the clock starts
+        t0 = time.perf_counter()
+        res = pool.map(_pyref_run, items, chunksize=1)
+        wall = time.perf_counter() - t0
+    reqs = sum(r["n"] for r in res)
+    mism = []
+    for k, (i, r) in enumerate(zip(sel, res)):
+        g = got_summ[i]
+        same = (int(g["ttft_met"]) == r["ttft_met"] and int(g["tpot_met"]) == r["tpot_met"]
+                and int(g["e2e_met"]) == r["e2e_met"] and int(g["worst_queue_wait_us"]) == r["worst"]
+                and (np.isnan(g["tps_p50"]) if r["p50"] is None else float(g["tps_p50"]) == r["p50"])
+                and (np.isnan(g["tps_p90"]) if r["p90"] is None else float(g["tps_p90"]) == r["p90"]))
+        if not same:
+            mism.append(int(i))
+    return {"value": reqs / wall, "unit": "simulated requests/s", "cores": min(threads, len(items)),
+            "kind": "reference", "cpu": cpu_model(),
+            "sample": f"{len(sel)} instances (stride {stride} over the {n_total} instances of {name}), "
+                      f"{reqs} requests, {wall:.1f} s wall; unmodified slosim.run from baseline/_ref, one process "
+                      f"per core; trace generation outside the timed region",
+            "per_instance_s_mean": float(np.mean([r["s"] for r in res])),
+            "parity": {"instances_checked": len(sel), "mismatched": mism[:10], "exact": not mism,
+                       "fields": "ttft/tpot/e2e met counts, p50/p90 tps, worst queue wait"}}
 
 
 # ---------------------------------------------------------- reference arm --
@@ -175,15 +318,13 @@ def run_reference(args):
     from oracle import oracle
 
     threads = os.cpu_count() or 1
-    n_total = N_CONFIG5 if args.workload == "config5" else (3072 if args.workload == "config3" else 2)
-    # per step: a bounded stride sample of the step's slice (~cpu_sample_s / steps seconds each)
-    per_step = {"config5": 1536, "config3": 768, "config2": 2}[args.workload]
+    n_total = N_TOTAL[args.workload]
+    slice_n = slice_size(args)
+    per_step = min(REF_SAMPLE[args.workload], slice_n)
     times, reqs = [], []
     for s in range(args.warmup + args.steps):
-        start = (s * args.slice) % n_total
-        sel = (start + np.sort(np.random.default_rng(s).choice(args.slice, per_step, replace=False))) % n_total
-        if args.workload == "config2":
-            sel = np.arange(2)
+        start = (s * slice_n) % n_total
+        sel = (start + np.sort(np.random.default_rng(s).choice(slice_n, per_step, replace=False))) % n_total
         sw = build_workload(args.workload, synth=oracle.synth, select=sel)
         t0 = time.perf_counter()
         oracle.run_batch(sw.packed, threads=threads)
@@ -198,21 +339,54 @@ def run_reference(args):
         "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * T / args.steps,
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "int64+f64",
         "data": "synthetic (reference LongTailSpec generator, host numpy)",
-        "config": dict(workload_meta(args.workload, args.slice), sample=f"{per_step} instances per step (seeded random sample of the step slice)"),
+        "config": dict(workload_meta(args.workload, slice_n),
+                       sample=f"{per_step} instances per step (seeded random sample of the step slice)"),
         "cpu_baseline": {"value": value, "unit": "simulated requests/s", "cores": threads, "kind": "port",
-                         "sample": f"{per_step} random instances/step x {args.steps} steps of {args.workload}, C oracle "
-                                   f"(oracle/slosim_oracle.c), {threads} threads"},
+                         "cpu": cpu_model(),
+                         "sample": f"{per_step} random instances/step x {args.steps} steps of {args.workload}, C "
+                                   f"oracle (oracle/slosim_oracle.c), {threads} threads"},
         "e2e": {"value": value, "unit": "simulated requests/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
     return 0
 
 
+# --------------------------------------------------------- rank launcher ---
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def launch_ranks(args):
+    """`--gpus N` without a torchrun environment: run N local ranks under torch.distributed.run."""
+    backend = os.environ.get("SLOSIM_DIST_BACKEND", "nccl")
+    if backend == "nccl":
+        import torch
+
+        n_dev = torch.cuda.device_count()
+        if n_dev < args.gpus:
+            print(f"bench.py: --gpus {args.gpus} but only {n_dev} CUDA device(s) visible", file=sys.stderr)
+            return 2
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr", "127.0.0.1", "--master-port", str(_free_port()), os.path.abspath(__file__)] + sys.argv[1:]
+    env = dict(os.environ, OMP_NUM_THREADS=os.environ.get("OMP_NUM_THREADS", "1"))
+    return subprocess.call(cmd, env=env)
+
+
 # ----------------------------------------------------------------- ours ---
-def main():
-    args = parse()
+def main(argv=None):
+    args = parse(argv)
+    world_env = os.environ.get("WORLD_SIZE")
+    if world_env is not None and int(world_env) != args.gpus:
+        print(f"bench.py: WORLD_SIZE={world_env} but --gpus {args.gpus}", file=sys.stderr)
+        return 2
     if args.impl == "reference":
         return run_reference(args)
+    if world_env is None and args.gpus > 1:
+        return launch_ranks(args)
     import torch
     import torch.distributed as dist
 
@@ -221,29 +395,33 @@ def main():
     from paper_2605_02329_b200.batch import DeviceBatch
 
     world, rank, local = dist_env()
-    dev = local % max(torch.cuda.device_count(), 1)
-    torch.cuda.set_device(dev)
     backend = os.environ.get("SLOSIM_DIST_BACKEND", "nccl")  # gloo: N ranks sharing one GPU (testing)
+    n_dev = torch.cuda.device_count()
+    if backend == "nccl" and n_dev < world:
+        print(f"bench.py: {world} ranks but only {n_dev} CUDA device(s)", file=sys.stderr)
+        return 2
+    dev = local % max(n_dev, 1)
+    torch.cuda.set_device(dev)
     if world > 1:
         if backend == "nccl":
             dist.init_process_group("nccl", device_id=torch.device("cuda", dev))
         else:
             dist.init_process_group(backend)
+        assert dist.get_world_size() == world
     L = _abi.lib()
 
     # full instance grid resident in HBM (instances + traces), summaries per instance
-    n_total = N_CONFIG5 if args.workload == "config5" else (3072 if args.workload == "config3" else 2)
-    slice_n = min(args.slice, n_total) if args.workload != "config2" else 2
+    n_total = N_TOTAL[args.workload]
+    slice_n = slice_size(args)
     n_slices = max(1, n_total // slice_n)
     t_pack = time.perf_counter()
     sw = build_workload(args.workload)
     pack_s = time.perf_counter() - t_pack
     db = DeviceBatch(sw.packed)
-    pk = sw.packed
-    n_pairs, n_slo, n_rates = {"config5": (4, 16, 64), "config3": (3, 16, 64), "config2": (2, 1, 1)}[args.workload]
+    n_pairs, n_slo, n_rates = GRID[args.workload]
     n_cells = n_pairs * n_slo * n_rates
     cells = torch.from_numpy(D.cell_ids_config_grid(np.arange(n_total), n_pairs, n_slo, n_rates)).cuda()
-    hist = torch.zeros(n_cells * 1001, dtype=torch.int64, device="cuda")
+    hist = torch.zeros(n_cells * N_BINS, dtype=torch.int64, device="cuda")
     flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
     stream = torch.cuda.current_stream()
 
@@ -274,7 +452,7 @@ def main():
     for s in timed:
         off = s * slice_n
         L.slosim_histogram(slice_n, ctypes.c_void_p(db.summaries.data_ptr() + off * 144),
-                           ctypes.c_void_p(cells.data_ptr() + off * 4), 1001, ctypes.c_void_p(hist.data_ptr()),
+                           ctypes.c_void_p(cells.data_ptr() + off * 4), N_BINS, ctypes.c_void_p(hist.data_ptr()),
                            ctypes.c_void_p(stream.cuda_stream))
     mine = torch.cat([db.summaries[s * slice_n * 144:(s + 1) * slice_n * 144] for s in timed])
     gathered, hist = D.exchange(mine, hist)
@@ -285,25 +463,42 @@ def main():
     clocks = clk.stop()
     elapsed_ms = t_start.elapsed_time(t_end)
     step_ms = [e0.elapsed_time(e1) for e0, e1 in ev]
-    tmax = torch.tensor([elapsed_ms], dtype=torch.float64, device="cuda" if backend == "nccl" else "cpu")
+    tdev = "cuda" if backend == "nccl" else "cpu"
+    tmax = torch.tensor([elapsed_ms, float(np.mean(step_ms))], dtype=torch.float64, device=tdev)
     if world > 1:
         dist.all_reduce(tmax, op=dist.ReduceOp.MAX)
-    elapsed_ms = float(tmax.item())
+    elapsed_ms, mean_ms_max = float(tmax[0].item()), float(tmax[1].item())
 
     host = db.summaries.cpu().numpy().view(_abi.summary_dtype())
     timed_idx = np.concatenate([np.arange(s * slice_n, (s + 1) * slice_n) for s in timed])
     summ = host[timed_idx]
     assert np.all(summ["status"] == 0), "engine reported a failed instance"
     reqs_rank = int(summ["n"].astype(np.int64).sum())
-    reqs_all = reqs_rank * world
+    rq = torch.tensor([reqs_rank], dtype=torch.int64, device=tdev)
+    if world > 1:
+        dist.all_reduce(rq, op=dist.ReduceOp.SUM)
+    reqs_all = int(rq.item())
     value = reqs_all / (elapsed_ms / 1e3)
+
+    # exchange evidence: every rank's rows arrive in rank order, the histogram counts every instance once
+    g_host = gathered.cpu().numpy()
+    h_host = hist.cpu().numpy()
+    n_rows = len(g_host) // 144
+    g_rows = g_host.view(_abi.summary_dtype()).copy()
+    g_rows["sim_cycles"] = 0  # clock diagnostics differ run to run; every other field is deterministic
+    exchange = {"ranks": world, "backend": backend if world > 1 else "none (1 rank)",
+                "rows_gathered": n_rows, "rows_expected": world * len(timed) * slice_n,
+                "own_rows_in_place": bool(np.array_equal(g_host[rank * len(mine):(rank + 1) * len(mine)],
+                                                         mine.cpu().numpy())),
+                "hist_total": int(h_host.sum()), "hist_sha16": hashlib.sha256(h_host.tobytes()).hexdigest()[:16],
+                "rows_sha16": hashlib.sha256(g_rows.tobytes()).hexdigest()[:16]}
 
     # roofline of the dominant kernel (sim_kernel): algorithmic bytes / mean launch duration
     peak, peak_kind = load_peaks()
     abytes = alg_bytes(summ) / len(timed)
     mean_ms = float(np.mean(step_ms))
     achieved = abytes / (mean_ms / 1e3) / 1e9
-    traffic, traffic_src, ncu_counters = profile_traffic(slice_n)
+    traffic, traffic_src, ncu_counters = profile_counters(slice_n)
     # compulsory floor of the byte model: the trace read (24 B/request) and the summary row (96 B/instance)
     floor_bytes = 24 * reqs_rank / len(timed) + 96 * slice_n
 
@@ -312,10 +507,17 @@ def main():
     if not args.no_e2e:
         e2e = measure_e2e(args, sw, timed, slice_n, world)
 
-    cpu = None
-    parity = None
+    cpu = parity = pyref = None
     if rank == 0 and not args.no_cpu:
         cpu, parity = cpu_baseline(args, host, timed[0], slice_n)
+        n_py = args.pyref_sample if args.pyref_sample >= 0 else {"config5": 64, "config3": 48, "config1": 12,
+                                                                  "config4": 16, "config2": 0}[args.workload]
+        if n_py > 0:
+            sel = np.arange(timed[0] * slice_n, (timed[0] + 1) * slice_n)
+            pyref = python_reference_baseline(args.workload, _sub_sweep(sw, sel), host[sel], n_py,
+                                              os.cpu_count() or 1)
+    if world > 1:
+        dist.barrier()
 
     if rank == 0:
         line = {
@@ -329,18 +531,32 @@ def main():
                          "frac": achieved / peak, "traffic": traffic,
                          "traffic_source": f"ncu dram__bytes_read+write per instance x {slice_n} ({traffic_src})",
                          "alg_bytes_per_launch": abytes, "mean_launch_ms": mean_ms,
-                         "floor_bytes_per_launch": floor_bytes, "ncu_counters": ncu_counters},
+                         "floor_bytes_per_launch": floor_bytes,
+                         "issue_frac": (ncu_counters or {}).get("smsp__issue_active_pct", 0) / 100 or None,
+                         "issue_note": "fraction of SMSP issue slots used by sim_kernel (ncu smsp__issue_active of "
+                                       "the committed capture): the path is issue/latency bound, not HBM bound",
+                         "ncu_counters": ncu_counters},
             "host_pack_s": round(pack_s, 2),
             "cpu_baseline": cpu,
+            "cpu_baseline_python": pyref,
             "parity": parity,
+            "exchange": exchange,
             "clocks": clocks,
-            "gpu_launches": 2 * len(timed) + len(timed),
+            "gpu_launches": 3 * len(timed),
             "kernel_ms_per_step": step_ms,
+            "mean_kernel_ms_max_over_ranks": mean_ms_max,
         }
         print(json.dumps(line), flush=True)
     if world > 1:
         dist.destroy_process_group()
     return 0
+
+
+def _sub_sweep(sw, sel):
+    """A view of the sweep restricted to `sel` (coords only; used by the Python reference baseline)."""
+    from paper_2605_02329_b200.batch import Sweep
+
+    return Sweep(sw.packed, sw.coords[sel], sw.traces, sw.name)
 
 
 def measure_e2e(args, sw, timed, slice_n, world):
@@ -364,7 +580,7 @@ def measure_e2e(args, sw, timed, slice_n, world):
         rc = _abi.lib().slosim_run_batch_host(ctypes.byref(b), ctypes.byref(kms))
         times.append(time.perf_counter() - t0)
         kernel_ms.append(round(kms.value, 1))
-        assert rc == 0
+        assert rc == 0, _abi.lib().slosim_last_error()
         reqs += part.n_requests
         h2d = arr.nbytes + inp.nbytes + out.nbytes + hit.nbytes + idr.nbytes + ctypes.sizeof(pk.profiles) + inst.nbytes
         d2h = part.summaries.nbytes
@@ -372,26 +588,29 @@ def measure_e2e(args, sw, timed, slice_n, world):
     import torch.distributed as dist
 
     on_gpu = not (dist.is_available() and dist.is_initialized()) or dist.get_backend() == "nccl"
-    t = torch.tensor([T], dtype=torch.float64, device="cuda" if on_gpu else "cpu")
+    t = torch.tensor([T, float(reqs)], dtype=torch.float64, device="cuda" if on_gpu else "cpu")
     if dist.is_available() and dist.is_initialized():
+        tr = t.clone()
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
-    return {"value": reqs * world / float(t.item()), "unit": "simulated requests/s", "h2d_bytes_per_step": h2d,
+        dist.all_reduce(tr, op=dist.ReduceOp.SUM)
+        reqs_all = float(tr[1].item())
+    else:
+        reqs_all = float(reqs)
+    return {"value": reqs_all / float(t[0].item()), "unit": "simulated requests/s", "h2d_bytes_per_step": h2d,
             "d2h_bytes_per_step": d2h, "entry_point": "slosim_run_batch_host (C-ABI, host buffers)",
             "wall_ms_per_step": [round(x * 1e3, 1) for x in times], "kernel_ms_per_step": kernel_ms}
 
 
 def cpu_baseline(args, host_summ, slice_id, slice_n):
-    """C oracle (port) on all host threads over a stride sample of one timed slice; bit-exact check."""
+    """C oracle (port) on all host threads over a sample of one timed slice; bit-exact check."""
     from oracle import oracle
 
     threads = os.cpu_count() or 1
-    n_total = N_CONFIG5 if args.workload == "config5" else (3072 if args.workload == "config3" else 2)
     # calibrate the sample to ~cpu_sample_s seconds: ~40k req/s per core for the port
-    target = int(args.cpu_sample_s * 40_000 * threads / 1000)
+    per_inst = {"config2": 100_000, "config4": 5_000}.get(args.workload, 1000)
+    target = int(args.cpu_sample_s * 40_000 * threads / per_inst)
     k = max(2, min(slice_n, target))
     sel = slice_id * slice_n + np.sort(np.random.default_rng(slice_id).choice(slice_n, k, replace=False))
-    if args.workload == "config2":
-        sel = np.arange(2)
     sw = build_workload(args.workload, synth=oracle.synth, select=sel)
     t0 = time.perf_counter()
     oracle.run_batch(sw.packed, threads=threads)
@@ -404,6 +623,7 @@ def cpu_baseline(args, host_summ, slice_id, slice_n):
         eq = np.array_equal(a, b, equal_nan=True) if a.dtype.kind == "f" else np.array_equal(a, b)
         mism += 0 if eq else 1
     cpu = {"value": sw.packed.n_requests / dt, "unit": "simulated requests/s", "cores": threads, "kind": "port",
+           "cpu": cpu_model(),
            "sample": f"{len(sel)} instances (seeded random sample of timed slice {slice_id}), "
                      f"{sw.packed.n_requests} requests, {dt:.1f} s"}
     parity = {"instances_checked": int(len(sel)), "fields_mismatched": int(mism),

@@ -20,7 +20,7 @@
 extern "C" {
 #endif
 
-#define SLOSIM_ABI_VERSION 1
+#define SLOSIM_ABI_VERSION 2
 
 /* Status codes: mirror the CLI exit codes of cli.py:1-5 (0 ok, 2 invalid input,
  * 3 configuration error — ConfigurationError domain.py:32-33). */
@@ -123,7 +123,10 @@ typedef struct slosim_traces {
 /* Per-instance result: MetricsReport (metrics.py:95-106) reduced to counts, plus
  * the decision digest and the byte-model counters of SURVEY §8(d). */
 typedef struct slosim_summary {
-    int32_t status;           /* SLOSIM_OK or SLOSIM_ECONFIG; bit 8 set: trace buffer overflow */
+    int32_t status;           /* SLOSIM_OK; SLOSIM_ECONFIG (unrunnable config, engine.py:218-232);
+                                 SLOSIM_EINVAL (malformed descriptor: n_requests > max_requests, profile_id
+                                 out of range, trace range outside the trace table, bad policy id, ...);
+                                 bit 8 set: trace buffer overflow */
     int32_t n;
     int32_t ttft_met, tpot_met, e2e_met, n_tps;
     double tps_p50, tps_p90;  /* NaN when no request has output_len >= 2 */
@@ -164,8 +167,11 @@ typedef struct slosim_batch {
     int64_t* trace_buf;       /* event-trace words (NULL = no tracing) */
     double* lut_out_sums;     /* optional final LUT per instance [n_instances][16*64] */
     int32_t* lut_out_counts;
-    int64_t max_requests;     /* max n_requests over instances (sizes the per-warp workspace) */
-    const int64_t* order;     /* optional processing order (permutation of instance ids); NULL = identity */
+    int64_t max_requests;     /* max n_requests over instances (sizes the per-warp workspace); <= 0: computed */
+    const int64_t* order;     /* optional processing order (permutation of instance ids); NULL = identity.
+                                 Entries outside [0, n_instances) are skipped. */
+    int64_t rows_capacity;    /* length of each rows.* array (0 = unchecked) */
+    int64_t trace_buf_capacity; /* words in trace_buf (0 = unchecked) */
 } slosim_batch_t;
 
 #define SLOSIM_F_ROWS 1          /* write per-request rows */
@@ -175,7 +181,12 @@ typedef struct slosim_batch {
 /* ---------------------------------------------------------------- engine ---
  * Replaces Simulation.run (engine.py:261-284) / run() (engine.py:416-420),
  * batched over instances (the qps x policy loop of cli.py:130-138).
- * All pointers in `batch` are DEVICE pointers; stream is a cudaStream_t. */
+ * All pointers in `batch` are DEVICE pointers; stream is a cudaStream_t.
+ * Stream-ordered: the call enqueues work and returns.  Every instance descriptor
+ * is validated on the device; a malformed one gets summary status SLOSIM_EINVAL
+ * and touches no memory outside its own summary row.  Launches on one device
+ * are serialised in stream order (a launch waits for the previous launch's
+ * completion, whatever stream it used), so concurrent callers are safe. */
 int slosim_run_batch(const slosim_batch_t* batch, void* stream);
 
 /* Same, with HOST pointers: copies in, runs, copies out, synchronizes.

@@ -150,6 +150,8 @@ class Batch(ctypes.Structure):
         ("lut_out_counts", c_void_p),
         ("max_requests", c_int64),
         ("order", c_void_p),
+        ("rows_capacity", c_int64),
+        ("trace_buf_capacity", c_int64),
     ]
 
 

@@ -227,6 +227,7 @@ class DeviceBatch:
         if self.rows is not None:
             for k, v in self.rows.items():
                 setattr(b.rows, k, v.data_ptr())
+            b.rows_capacity = int(self.rows["ttft_us"].numel())
         b.max_requests = int(packed.instances["n_requests"].max()) if packed.n_instances else 0
         self.order = t(schedule_order(packed.instances) if order is None else order)
         b.order = self.order.data_ptr()

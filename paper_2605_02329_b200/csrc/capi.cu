@@ -37,16 +37,18 @@ int fail_cuda(cudaError_t e, const char* what) {
         if (e_ != cudaSuccess) return fail_cuda(e_, #call);   \
     } while (0)
 
-// Grow-only device arena per purpose (the engine workspace, profile tables, snapshot scratch).
+// Grow-only device arena per purpose (the engine workspace, profile tables,
+// work counter, snapshot scratch, host-entry staging), one set per device.
 struct Arena {
     void* ptr = nullptr;
     size_t size = 0;
-    int device = -1;
-    cudaError_t reserve(size_t bytes) {
-        int dev = 0;
-        cudaGetDevice(&dev);
-        if (ptr && size >= bytes && dev == device) return cudaSuccess;
-        if (ptr && dev == device) cudaFree(ptr);
+    // `busy`: last stream work that used the arena (waited on before it is freed)
+    cudaError_t reserve(size_t bytes, cudaEvent_t busy = nullptr) {
+        if (ptr && size >= bytes) return cudaSuccess;
+        if (ptr) {
+            if (busy) cudaEventSynchronize(busy);
+            cudaFree(ptr);
+        }
         ptr = nullptr;
         size = 0;
         size_t want = std::max(bytes, (size_t)1 << 20);
@@ -55,32 +57,50 @@ struct Arena {
         // zero once per allocation: the engine's branch-free LUT update reads (and discards) the
         // neighbour of an edge cell, which may lie outside the live part of a workspace LUT
         e = cudaMemset(ptr, 0, want);
-        if (e != cudaSuccess) return e;
+        if (e != cudaSuccess) { cudaFree(ptr); ptr = nullptr; return e; }
         size = want;
-        device = dev;
         return cudaSuccess;
     }
 };
-Arena g_ws, g_tabs, g_work, g_snap;
 
-int g_sms = 0, g_blocks_per_sm = 0;
+// Per-device library state.  Engine launches on one device are serialised in
+// stream order: each launch waits for the previous launch's `done` event
+// (whatever stream it ran on) before it rewrites the shared workspace, profile
+// tables and work counter, so concurrent callers on different streams get the
+// results of sequential calls.
+constexpr int kMaxDevices = 64;
+struct DevState {
+    Arena ws, tabs, work, snap, io;
+    int sms = 0, blocks_per_sm = 0;
+    cudaEvent_t done = nullptr;
+};
+DevState g_dev[kMaxDevices];
 
-int launch_geometry(int64_t n_instances, int* grid) {
-    if (!g_sms) {
-        int dev = 0;
-        CK(cudaGetDevice(&dev));
-        CK(cudaDeviceGetAttribute(&g_sms, cudaDevAttrMultiProcessorCount, dev));
-        CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&g_blocks_per_sm, sim_kernel, 128, 0));
-        if (g_blocks_per_sm < 1) g_blocks_per_sm = 1;
+int current_device(int* dev) {
+    CK(cudaGetDevice(dev));
+    if (*dev < 0 || *dev >= kMaxDevices) {
+        snprintf(g_err, sizeof(g_err), "device %d beyond the library limit (%d)", *dev, kMaxDevices);
+        return SLOSIM_ECUDA;
+    }
+    return SLOSIM_OK;
+}
+
+DevState& dev_state(int dev) { return g_dev[dev]; }
+
+int launch_geometry(DevState& ds, int dev, int64_t n_instances, int* grid) {
+    if (!ds.sms) {
+        CK(cudaDeviceGetAttribute(&ds.sms, cudaDevAttrMultiProcessorCount, dev));
+        CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&ds.blocks_per_sm, sim_kernel, 128, 0));
+        if (ds.blocks_per_sm < 1) ds.blocks_per_sm = 1;
         // experiment knob: fewer resident blocks per SM (occupancy studies)
         if (const char* e = getenv("SLOSIM_BLOCKS_PER_SM")) {
             int v = atoi(e);
-            if (v >= 1 && v < g_blocks_per_sm) g_blocks_per_sm = v;
+            if (v >= 1 && v < ds.blocks_per_sm) ds.blocks_per_sm = v;
         }
     }
     int64_t warps_needed = n_instances;
     int64_t blocks = (warps_needed + 3) / 4;
-    int64_t full = (int64_t)g_sms * g_blocks_per_sm;
+    int64_t full = (int64_t)ds.sms * ds.blocks_per_sm;
     *grid = (int)std::max<int64_t>(1, std::min<int64_t>(blocks, full));
     return SLOSIM_OK;
 }
@@ -89,17 +109,22 @@ int launch_geometry(int64_t n_instances, int* grid) {
 
 // ------------------------------------------------------------------ engine --
 extern "C" int64_t slosim_workspace_bytes(const slosim_batch_t* b) {
-    if (!b) return -1;
-    int grid = 0;
-    if (launch_geometry(b->n_instances, &grid) != SLOSIM_OK) return -1;
+    if (!b || b->n_instances < 0) return -1;
+    int dev = 0, grid = 0;
+    if (current_device(&dev) != SLOSIM_OK) return -1;
+    if (launch_geometry(dev_state(dev), dev, b->n_instances, &grid) != SLOSIM_OK) return -1;
     return (int64_t)grid * 4 * (int64_t)ws_bytes(b->max_requests) +
            (int64_t)b->n_profiles * 2 * (int64_t)sizeof(LutMem);
 }
 
 extern "C" int slosim_run_batch(const slosim_batch_t* b, void* stream) {
-    if (!b || b->n_instances < 0 || b->n_profiles < 1 || !b->profiles || !b->instances || !b->summaries)
+    if (!b || b->n_instances < 0 || b->n_profiles < 1 || !b->profiles || !b->instances || !b->summaries ||
+        b->traces.n_total < 0)
         return SLOSIM_EINVAL;
     if (b->n_instances == 0) return SLOSIM_OK;
+    if (b->traces.n_total > 0 && (!b->traces.arrival_us || !b->traces.input_len || !b->traces.output_len ||
+                                  !b->traces.prefix_hit_len || !b->traces.id_rank))
+        return SLOSIM_EINVAL;
     if ((b->flags & SLOSIM_F_ROWS) &&
         (!b->rows.ttft_us || !b->rows.mean_tpot_us || !b->rows.decode_tps || !b->rows.met_flags ||
          !b->rows.deadline_misses || !b->rows.t_prefill_finish || !b->rows.t_first_token ||
@@ -108,6 +133,11 @@ extern "C" int slosim_run_batch(const slosim_batch_t* b, void* stream) {
     if ((b->flags & SLOSIM_F_EXPORT_LUT) && (!b->lut_out_sums || !b->lut_out_counts)) return SLOSIM_EINVAL;
     cudaStream_t st = (cudaStream_t)stream;
     std::lock_guard<std::mutex> lock(g_mu);
+    int dev = 0;
+    int rc = current_device(&dev);
+    if (rc) return rc;
+    DevState& ds = dev_state(dev);
+    if (!ds.done) CK(cudaEventCreateWithFlags(&ds.done, cudaEventDisableTiming));
     int64_t cap = b->max_requests;
     if (cap <= 0) {
         std::vector<slosim_instance_t> h((size_t)b->n_instances);
@@ -115,39 +145,44 @@ extern "C" int slosim_run_batch(const slosim_batch_t* b, void* stream) {
         CK(cudaStreamSynchronize(st));
         for (auto& x : h) cap = std::max<int64_t>(cap, x.n_requests);
     }
+    if (cap > INT32_MAX) return SLOSIM_EINVAL;
     int grid = 0;
-    int rc = launch_geometry(b->n_instances, &grid);
+    rc = launch_geometry(ds, dev, b->n_instances, &grid);
     if (rc) return rc;
     size_t stride = ws_bytes(cap);
     size_t total = stride * (size_t)grid * 4;
-    CK(g_ws.reserve(total));
-    CK(g_tabs.reserve(sizeof(LutMem) * 2 * (size_t)b->n_profiles));
-    CK(g_work.reserve(64));
-    LutMem* sched = (LutMem*)g_tabs.ptr;
+    CK(ds.ws.reserve(total, ds.done));
+    CK(ds.tabs.reserve(sizeof(LutMem) * 2 * (size_t)b->n_profiles, ds.done));
+    CK(ds.work.reserve(64, ds.done));
+    // the previous launch on this device (any stream) owns the arenas until it completes
+    CK(cudaStreamWaitEvent(st, ds.done, 0));
+    LutMem* sched = (LutMem*)ds.tabs.ptr;
     LutMem* frozen = sched + b->n_profiles;
     build_profile_tables<<<b->n_profiles, 32, 0, st>>>(b->profiles, b->n_profiles, sched, frozen);
     CK(cudaGetLastError());
-    CK(cudaMemsetAsync(g_work.ptr, 0, 8, st));
+    CK(cudaMemsetAsync(ds.work.ptr, 0, 8, st));
     Ctx cx;
     cx.B = *b;
+    cx.B.max_requests = cap;
     cx.sched_tab = sched;
     cx.frozen_tab = frozen;
     const bool force_lat = getenv("SLOSIM_FORCE_LATENCY_ENGINE") != nullptr;  // experiment knob
-    if ((b->n_instances <= (int64_t)g_sms * 4 || force_lat) && !getenv("SLOSIM_NO_LATENCY_ENGINE")) {
+    if ((b->n_instances <= (int64_t)ds.sms * 4 || force_lat) && !getenv("SLOSIM_NO_LATENCY_ENGINE")) {
         // at most one 4-warp block per SM: the spill-free latency build (engine_lat.cu)
-        CK(slosim_launch_latency_engine(grid, &cx, (char*)g_ws.ptr, stride, cap, (unsigned long long*)g_work.ptr, st));
+        CK(slosim_launch_latency_engine(grid, &cx, (char*)ds.ws.ptr, stride, cap, (unsigned long long*)ds.work.ptr,
+                                        st));
     } else {
-        sim_kernel<<<grid, 128, 0, st>>>(cx, (char*)g_ws.ptr, stride, cap, (unsigned long long*)g_work.ptr);
+        sim_kernel<<<grid, 128, 0, st>>>(cx, (char*)ds.ws.ptr, stride, cap, (unsigned long long*)ds.work.ptr);
         CK(cudaGetLastError());
     }
+    CK(cudaEventRecord(ds.done, st));
     return SLOSIM_OK;
 }
 
 namespace {
-// Device staging for the host-buffer entry point: one grow-only arena carved
-// into 256-byte-aligned pieces (no cudaMalloc/cudaFree per call, so a call
-// costs its copies and kernels only).
-Arena g_io;
+// Device staging for the host-buffer entry point: one grow-only arena per
+// device carved into 256-byte-aligned pieces (no cudaMalloc/cudaFree per call,
+// so a call costs its copies and kernels only).
 std::mutex g_io_mu;
 struct Carve {
     char* base = nullptr;
@@ -193,6 +228,9 @@ static void default_order(const slosim_batch_t* hb, std::vector<int64_t>& order)
 extern "C" int slosim_run_batch_host(const slosim_batch_t* hb, float* elapsed_ms) {
     if (!hb) return SLOSIM_EINVAL;
     std::lock_guard<std::mutex> lock(g_io_mu);
+    int dev = 0;
+    if (int rc0 = current_device(&dev)) return rc0;
+    Arena& io = dev_state(dev).io;
     slosim_batch_t d = *hb;
     size_t nt = (size_t)hb->traces.n_total, ni = (size_t)hb->n_instances;
     int64_t rows_n = 0, tb_n = 0;
@@ -214,8 +252,8 @@ extern "C" int slosim_run_batch_host(const slosim_batch_t* hb, float* elapsed_ms
     for (int pass = 0; pass < 2; pass++) {
         Carve c;
         if (pass == 1) {
-            CK(g_io.reserve(0));
-            c.base = (char*)g_io.ptr;
+            CK(io.reserve(0));
+            c.base = (char*)io.ptr;
         }
         d.traces.arrival_us = c.take<int64_t>(nt);
         d.traces.input_len = c.take<int32_t>(nt);
@@ -238,7 +276,7 @@ extern "C" int slosim_run_batch_host(const slosim_batch_t* hb, float* elapsed_ms
         d.lut_out_sums = c.take<double>(lut ? ni * FR : 0);
         d.lut_out_counts = c.take<int32_t>(lut ? ni * FR : 0);
         d.order = c.take<int64_t>(ni);
-        if (pass == 0) CK(g_io.reserve(c.off));
+        if (pass == 0) CK(io.reserve(c.off));
     }
     CK(up((int64_t*)d.traces.arrival_us, hb->traces.arrival_us, nt));
     CK(up((int32_t*)d.traces.input_len, hb->traces.input_len, nt));
@@ -543,7 +581,18 @@ struct Bump {
     }
 };
 
-cudaError_t snap_reserve(size_t bytes) { return g_snap.reserve(bytes); }
+// Snapshot scratch of the current device (snapshot calls are synchronous).
+char* g_snap_ptr = nullptr;
+cudaError_t snap_reserve(size_t bytes) {
+    int dev = 0;
+    cudaError_t e = cudaGetDevice(&dev);
+    if (e != cudaSuccess) return e;
+    if (dev < 0 || dev >= kMaxDevices) return cudaErrorInvalidDevice;
+    Arena& a = g_dev[dev].snap;
+    e = a.reserve(bytes);
+    g_snap_ptr = (char*)a.ptr;
+    return e;
+}
 
 SnapLut make_snaplut(int32_t nb, const int32_t* bb, int32_t ns, const int32_t* sb) {
     SnapLut s{};
@@ -588,7 +637,7 @@ extern "C" int slosim_lut_lookup(int32_t nb, const int32_t* bb, int32_t ns, cons
     std::vector<int32_t> fc;
     frame(nb, ns, sums, counts, fs, fc);
     CK(snap_reserve(sizeof(LutMem) + fs.size() * 12 + (size_t)n * 24 + 4096));
-    Bump bp{(char*)g_snap.ptr};
+    Bump bp{g_snap_ptr};
     LutMem* tab = bp.take<LutMem>(1);
     double* dfs = bp.take<double>(fs.size());
     int32_t* dfc = bp.take<int32_t>(fc.size());
@@ -608,7 +657,7 @@ extern "C" int slosim_decode_formula(int32_t n_base, const int64_t* bx, const do
     if (n == 0) return SLOSIM_OK;
     std::lock_guard<std::mutex> lock(g_mu);
     CK(snap_reserve((size_t)n * 24 + 4096));
-    Bump bp{(char*)g_snap.ptr};
+    Bump bp{g_snap_ptr};
     int64_t* dbx = bp.take<int64_t>(n_base);
     double* dby = bp.take<double>(n_base);
     int64_t* db = bp.take<int64_t>(n);
@@ -628,7 +677,7 @@ extern "C" int slosim_estimate_duration(int64_t total_tokens, int64_t total_busy
     if (n == 0) return SLOSIM_OK;
     std::lock_guard<std::mutex> lock(g_mu);
     CK(snap_reserve((size_t)n * 16 + 4096));
-    Bump bp{(char*)g_snap.ptr};
+    Bump bp{g_snap_ptr};
     int64_t* dt = bp.take<int64_t>(n);
     int64_t* dout = bp.take<int64_t>(n);
     H2D(dt, tokens, n);
@@ -645,7 +694,7 @@ extern "C" int slosim_predict_finish(int32_t n, const int64_t* arrival, const in
     if (n == 0) return SLOSIM_OK;
     std::lock_guard<std::mutex> lock(g_mu);
     CK(snap_reserve((size_t)n * 24 + 4096));
-    Bump bp{(char*)g_snap.ptr};
+    Bump bp{g_snap_ptr};
     int64_t* da = bp.take<int64_t>(n);
     int64_t* dr = bp.take<int64_t>(n);
     int64_t* dout = bp.take<int64_t>(n);
@@ -666,7 +715,7 @@ extern "C" int slosim_select_prefill(int32_t policy, int32_t n, const int64_t* a
     std::lock_guard<std::mutex> lock(g_mu);
     size_t wsb = ws_bytes(n);
     CK(snap_reserve(wsb + (size_t)n * 64 + 8192));
-    Bump bp{(char*)g_snap.ptr};
+    Bump bp{g_snap_ptr};
     char* dws = bp.take<char>(wsb);
     int64_t* da = bp.take<int64_t>(n);
     int32_t* di = bp.take<int32_t>(n);
@@ -703,7 +752,7 @@ extern "C" int slosim_select_decode(int32_t policy, int32_t n, const int64_t* se
     frame(nb, ns, sums, counts, fs, fc);
     size_t wsb = ws_bytes(n);
     CK(snap_reserve(wsb + sizeof(LutMem) + fs.size() * 12 + (size_t)n * 64 + 8192));
-    Bump bp{(char*)g_snap.ptr};
+    Bump bp{g_snap_ptr};
     char* dws = bp.take<char>(wsb);
     LutMem* tab = bp.take<LutMem>(1);
     double* dfs = bp.take<double>(fs.size());
@@ -738,7 +787,7 @@ extern "C" int slosim_prefill_batch_us(int32_t n_curve, const int64_t* cx, const
     if (n_curve < 2 || n_curve > SLOSIM_MAX_CURVE_POINTS || k < 0) return SLOSIM_EINVAL;
     std::lock_guard<std::mutex> lock(g_mu);
     CK(snap_reserve((size_t)(k + 1) * 16 + 8192));
-    Bump bp{(char*)g_snap.ptr};
+    Bump bp{g_snap_ptr};
     int64_t* dx = bp.take<int64_t>(n_curve);
     int64_t* dy = bp.take<int64_t>(n_curve);
     int64_t* dd = bp.take<int64_t>(k + 1);
@@ -765,7 +814,7 @@ extern "C" int slosim_request_metrics(int64_t n, const double* arrival, const in
     for (int64_t k = 0; k < n; k++) if (ts_offsets[k + 1] - ts_offsets[k] < 1) return SLOSIM_EINVAL;
     std::lock_guard<std::mutex> lock(g_mu);
     CK(snap_reserve((size_t)n * 80 + (size_t)nts * 8 + 8192));
-    Bump bp{(char*)g_snap.ptr};
+    Bump bp{g_snap_ptr};
     double* da = bp.take<double>(n);
     int64_t* dol = bp.take<int64_t>(n);
     int64_t* doff = bp.take<int64_t>(n + 1);
@@ -802,7 +851,7 @@ extern "C" int slosim_synth_profile(slosim_profile_t* profile, int32_t n_anchors
     if (nbase == 0 || nbase > SLOSIM_MAX_BASE_POINTS) return SLOSIM_EINVAL;
     std::lock_guard<std::mutex> lock(g_mu);
     CK(snap_reserve(sizeof(slosim_profile_t) + (size_t)n_anchors * 24 + 8192));
-    Bump bp{(char*)g_snap.ptr};
+    Bump bp{g_snap_ptr};
     slosim_profile_t* dp = bp.take<slosim_profile_t>(1);
     int64_t* dab = bp.take<int64_t>(n_anchors);
     int64_t* das = bp.take<int64_t>(n_anchors);
@@ -844,7 +893,7 @@ extern "C" int slosim_device_count(void) {
 }
 
 extern "C" const char* slosim_build_info(void) {
-    return "slosim_b200 abi=" "1" " arch=sm_100a fmad=false";
+    return "slosim_b200 abi=2 arch=sm_100a fmad=false";
 }
 
 extern "C" const char* slosim_last_error(void) { return g_err; }
@@ -902,9 +951,13 @@ extern "C" int slosim_exchange(void* nccl_comm, const slosim_summary_t* d_mine, 
 }
 
 #ifdef SLOSIM_PROF
-// Debug builds only: read (and optionally reset) the section-profile counters of the engine loop.
+cudaError_t slosim_lat_prof_read(unsigned long long* out16, int reset);
+// Debug builds only: read (and optionally reset) the section-profile counters of both engine builds.
 extern "C" int slosim_prof_read(unsigned long long* out16, int reset) {
+    unsigned long long lat[16];
     CK(cudaMemcpyFromSymbol(out16, slosim::g_prof, 16 * sizeof(unsigned long long)));
+    CK(slosim_lat_prof_read(lat, reset));
+    for (int k = 0; k < 16; k++) out16[k] += lat[k];
     if (reset) {
         unsigned long long z[16] = {0};
         CK(cudaMemcpyToSymbol(slosim::g_prof, z, sizeof(z)));

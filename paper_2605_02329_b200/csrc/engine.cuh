@@ -100,6 +100,14 @@ __global__ void build_profile_tables(const slosim_profile_t* profiles, int n_pro
     int p = blockIdx.x;
     if (p >= n_profiles) return;
     const slosim_profile_t* P = profiles + p;
+    // a malformed profile (grid or curve sizes beyond the frame) is marked bad: its instances get EINVAL
+    const bool ok = P->nb >= 1 && P->nb <= SLOSIM_MAX_BSZ_BUCKETS && P->ns >= 1 && P->ns <= SLOSIM_MAX_SEQ_BUCKETS &&
+                    P->n_curve >= 2 && P->n_curve <= SLOSIM_MAX_CURVE_POINTS && P->n_base >= 0 &&
+                    P->n_base <= SLOSIM_MAX_BASE_POINTS && (P->n_base >= 1 || P->gt_frozen);
+    if (!ok) {
+        if (lane == 0) { sched[p].bad = 1; frozen[p].bad = 1; }
+        return;
+    }
     lut_build(sched + p, P->nb, P->ns, P->bsz_buckets, P->seq_buckets, P->lut_sums, P->lut_counts, lane);
     lut_build(frozen + p, P->nb, P->ns, P->bsz_buckets, P->seq_buckets, P->gt_sums, P->gt_counts, lane);
 }
@@ -455,9 +463,9 @@ __device__ __noinline__ double radix_select(const double* v, int n, int64_t r, i
     return __longlong_as_double((long long)prefix);
 }
 
-__device__ void write_config_error(slosim_summary_t* out, int n) {
+__device__ void write_status(slosim_summary_t* out, int n, int status) {
     slosim_summary_t s = {};
-    s.status = SLOSIM_ECONFIG;
+    s.status = status;
     s.n = n;
     s.tps_p50 = __longlong_as_double(0x7ff8000000000000LL);
     s.tps_p90 = s.tps_p50;
@@ -1337,6 +1345,24 @@ __device__ __noinline__ int ff_steps(Sim& S, Slot& sl, int64_t t, int lane) {
 #define SKIP_SINGLE(an) ((an) > 1)
 #endif
 
+// Descriptor validation (include/slosim_b200.h): everything the engine indexes
+// with must lie inside the buffers the batch describes.
+__device__ __noinline__ bool instance_ok(const slosim_batch_t* B, const slosim_instance_t* I, const LutMem* tabs) {
+    const int64_t n = I->n_requests, off = I->trace_offset;
+    bool ok = n >= 0 && n <= B->max_requests && I->profile_id >= 0 && I->profile_id < B->n_profiles &&
+              off >= 0 && off <= B->traces.n_total - n && I->prefill_policy >= 0 && I->prefill_policy <= 2 &&
+              I->decode_policy >= 0 && I->decode_policy <= 1 && I->chunk_budget >= 1 && I->ttft_slo_us > 0 &&
+              I->tpot_slo_us > 0 && I->kv_capacity_tokens >= 1 && I->transfer_base_us >= 0 &&
+              I->transfer_per_token_us >= 0.0 && !(I->rescale_factor != I->rescale_factor);
+    if (ok) ok = tabs[I->profile_id].bad == 0;
+    if (ok && (B->flags & SLOSIM_F_ROWS))
+        ok = I->row_offset >= 0 && (B->rows_capacity <= 0 || I->row_offset <= B->rows_capacity - n);
+    if (ok && B->trace_buf && I->trace_buf_offset >= 0)
+        ok = I->trace_buf_words >= 0 &&
+             (B->trace_buf_capacity <= 0 || I->trace_buf_offset <= B->trace_buf_capacity - I->trace_buf_words);
+    return ok;
+}
+
 // DP: decode policy (compile-time), FULL: event trace / per-request rows / LUT
 // export compiled in, G: power-of-two LUT geometry.  The throughput path runs
 // simulate<DP, false, G>, whose hot loop carries no tracing or row-output code.
@@ -1355,8 +1381,13 @@ __device__ SIM_INLINE void simulate(const Ctx& cx, int64_t ii, const WS& w, int 
     const slosim_instance_t* I = S.I;
     S.n = I->n_requests;
     const int pid = I->profile_id;
-    S.P = S.B->profiles + pid;
     const int64_t off = I->trace_offset;
+    // C-ABI contract: a malformed descriptor gets SLOSIM_EINVAL and touches nothing else
+    if (!instance_ok(S.B, I, cx.sched_tab)) {
+        if (lane == 0) write_status(S.B->summaries + ii, S.n, SLOSIM_EINVAL);
+        return;
+    }
+    S.P = S.B->profiles + pid;
     S.Tarr = S.B->traces.arrival_us + off;
     S.Tinp = S.B->traces.input_len + off;
     S.Tout = S.B->traces.output_len + off;
@@ -1381,7 +1412,7 @@ __device__ SIM_INLINE void simulate(const Ctx& cx, int64_t ii, const WS& w, int 
     worst = wmax64(worst);
     const LutMem* ST = cx.sched_tab + pid;
     if (worst > S.kv_cap || ST->rowmask == 0) {
-        if (lane == 0) write_config_error(S.B->summaries + ii, S.n);
+        if (lane == 0) write_status(S.B->summaries + ii, S.n, SLOSIM_ECONFIG);
         return;
     }
     const bool use_lut = DP == SLOSIM_DECODE_KAIROS_SLACK || (S.B->flags & (SLOSIM_F_ALWAYS_LUT | SLOSIM_F_EXPORT_LUT));
@@ -1667,13 +1698,15 @@ __global__ void __launch_bounds__(128, SLOSIM_MIN_BLOCKS)
         k = __shfl_sync(FULLMASK, k, 0);
         if ((int64_t)k >= N) break;
         const int64_t ii = cx.B.order ? cx.B.order[k] : (int64_t)k;
+        if (ii < 0 || ii >= N) continue;  // not a permutation entry: skipped (C-ABI contract)
         const slosim_instance_t* I = cx.B.instances + ii;
         const bool kairos = I->decode_policy == SLOSIM_DECODE_KAIROS_SLACK;
+        const bool pid_ok = I->profile_id >= 0 && I->profile_id < cx.B.n_profiles;
         // power-of-two LUT geometry: index arithmetic and exact power-of-two divisions
 #ifdef SLOSIM_NO_GEO
         const bool geo = false;
 #else
-        const bool geo = cx.sched_tab[I->profile_id].geo != 0;
+        const bool geo = pid_ok && cx.sched_tab[I->profile_id].geo != 0;
 #endif
         if (full) {
             if (kairos) {

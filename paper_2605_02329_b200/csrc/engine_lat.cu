@@ -26,3 +26,15 @@ cudaError_t slosim_launch_latency_engine(int grid, const void* cx, char* ws, siz
     slosim_lat::sim_kernel<<<grid, 128, 0, st>>>(c, ws, stride, cap, work);
     return cudaGetLastError();
 }
+
+#ifdef SLOSIM_PROF
+// Section-profile counters of the latency build (summed with the throughput build's by slosim_prof_read).
+cudaError_t slosim_lat_prof_read(unsigned long long* out16, int reset) {
+    cudaError_t e = cudaMemcpyFromSymbol(out16, slosim_lat::g_prof, 16 * sizeof(unsigned long long));
+    if (e == cudaSuccess && reset) {
+        unsigned long long z[16] = {0};
+        e = cudaMemcpyToSymbol(slosim_lat::g_prof, z, sizeof(z));
+    }
+    return e;
+}
+#endif

@@ -35,6 +35,7 @@ struct LutMem {
     int32_t populated;
     int32_t geo;  // 1: bsz buckets 2^0..2^(nb-1) and seq buckets (j+1) << wsh (index math, no tables)
     int32_t wsh;
+    int32_t bad;  // 1: the profile is malformed (build_profile_tables)
     uint8_t bidx[264];  // bidx[b] = bisect_left(bb, b), b <= 256
     uint8_t sidx[264];  // sidx[q] = bisect_left(sb, q << sshift), q <= 256
 };
@@ -134,6 +135,7 @@ __device__ void lut_build(LutMem* L, int nb, int ns, const int32_t* bb, const in
         L->full = cells == nb * ns;
         L->geo = geo ? 1 : 0;
         L->wsh = wsh;
+        L->bad = 0;
     }
     __syncwarp();
 }

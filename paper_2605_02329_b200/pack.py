@@ -172,7 +172,9 @@ class PackedBatch:
         if self.rows is not None:
             for k, v in self.rows.items():
                 setattr(b.rows, k, v.ctypes.data)
+            b.rows_capacity = len(self.rows["ttft_us"])
         b.trace_buf = self.trace_buf.ctypes.data if self.trace_buf is not None else None
+        b.trace_buf_capacity = len(self.trace_buf) if self.trace_buf is not None else 0
         if self.lut_out_sums is not None:
             b.lut_out_sums = self.lut_out_sums.ctypes.data
             b.lut_out_counts = self.lut_out_counts.ctypes.data

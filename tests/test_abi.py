@@ -35,7 +35,7 @@ def test_library_exports_all_header_symbols():
     # loading needs no GPU; calling compute does
     lib = ctypes.CDLL(_abi.LIB_PATH)
     lib.slosim_abi_version.restype = ctypes.c_int
-    assert lib.slosim_abi_version() == 1
+    assert lib.slosim_abi_version() == 2
 
 
 def test_lib_fails_loudly_without_device():
@@ -64,6 +64,7 @@ int main(void) {
   P(slosim_instance_t, row_offset) P(slosim_instance_t, trace_buf_words)
   P(slosim_summary_t, tps_p50) P(slosim_summary_t, digest) P(slosim_summary_t, max_active)
   P(slosim_batch_t, profiles) P(slosim_batch_t, instances) P(slosim_batch_t, rows) P(slosim_batch_t, max_requests)
+  P(slosim_batch_t, order) P(slosim_batch_t, rows_capacity) P(slosim_batch_t, trace_buf_capacity)
   return 0;
 }
 """

@@ -139,22 +139,64 @@ def _summaries_equal(got, want):
         assert eq, k
 
 
-def test_gpu_equals_oracle_on_config2_and_config4_samples(lib):
-    """SURVEY Appendix B configs 2 (one 100k-request instance per pair) and 4 (5k-request
-    round-robin sub-traces): GPU vs oracle, all summary fields bit-exact."""
+# SURVEY Appendix C, config 2 (100k requests, qps 1.0), computed from the unmodified reference:
+# (e2e, ttft, tpot attainment to 4 decimals, p50 decode tok/s exact)
+APPENDIX_C_CONFIG2 = {("kairos-urgency", "kairos-slack"): (0.9483, 0.9667, 0.9718, 69.80149783567873),
+                      ("fcfs", "continuous"): (0.8212, 0.8601, 0.9357, 52.09747110032166)}
+
+
+def test_gpu_equals_oracle_and_appendix_c_on_config2(lib):
+    """SURVEY Appendix B config 2 (one 100k-request instance per pair): GPU vs oracle, all summary
+    fields bit-exact, and the reference's own config-2 numbers of SURVEY Appendix C."""
     from oracle import oracle
-    from paper_2605_02329_b200.batch import config2, config4, run_batch
+    from paper_2605_02329_b200.batch import PAIRS_2, config2, run_batch
 
     sw = config2()
     got = run_batch(sw.packed).copy()
     ref = config2(synth=oracle.synth)
     oracle.run_batch(ref.packed, threads=2)
     _summaries_equal(got, ref.packed.summaries)
+    for i, pair in enumerate(PAIRS_2[::-1]):
+        e2e, ttft, tpot, p50 = APPENDIX_C_CONFIG2[pair]
+        g = got[i]
+        n = int(g["n"])
+        assert n == 100_000 and g["status"] == 0
+        # Python int/int division and Python round(), as the reference's aggregate + the survey table
+        att = tuple(round(int(g[k]) / n, 4) for k in ("e2e_met", "ttft_met", "tpot_met"))
+        assert att == (e2e, ttft, tpot), (pair, att)
+        assert float(g["tps_p50"]) == p50, pair
 
-    kw = dict(seeds=range(3), n_requests=20_000)
-    sel = np.arange(0, 24, 5)
-    sw = config4(select=sel, **kw)
+
+def test_gpu_equals_oracle_on_full_config4(lib):
+    """SURVEY Appendix B config 4 in full: 256 seeds x 20k requests at qps 4.0, each split
+    round-robin into four 5k-request 1P+1D pairs, x 2 policy pairs = 2048 instances (10.2M
+    simulated requests), GPU vs oracle on every summary field."""
+    import os
+
+    from oracle import oracle
+    from paper_2605_02329_b200.batch import config4, run_batch
+
+    sw = config4()
     got = run_batch(sw.packed).copy()
-    ref = config4(select=sel, synth=oracle.synth, **kw)
-    oracle.run_batch(ref.packed, threads=8)
+    ref = config4(synth=oracle.synth)
+    oracle.run_batch(ref.packed, threads=os.cpu_count() or 8)
+    assert np.all(got["status"] == 0)
+    _summaries_equal(got, ref.packed.summaries)
+
+
+def test_gpu_equals_oracle_on_config5_stride_sample(lib):
+    """SURVEY §8(c) parity procedure for config 5: a 1/4096 stride sample (256 instances spread over
+    252 of the 256 seeds, every rate, SLO scale and policy pair) in one launch, GPU vs oracle bit-exact."""
+    import os
+
+    from oracle import oracle
+    from paper_2605_02329_b200.batch import config5, run_batch
+
+    sel = (np.arange(256, dtype=np.int64) * 4165 + 1337) % (1 << 20)  # stride 4165: every pair, SLO scale and rate
+    sw = config5(select=sel)
+    got = run_batch(sw.packed).copy()
+    ref = config5(select=sel, synth=oracle.synth)
+    oracle.run_batch(ref.packed, threads=os.cpu_count() or 8)
+    assert len(set(sw.coords["trace"].tolist())) == 252
+    assert len(set(sw.coords["pair"].tolist())) == 4 and len(set(sw.coords["rate"].tolist())) == 64
     _summaries_equal(got, ref.packed.summaries)
