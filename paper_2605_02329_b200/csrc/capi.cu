@@ -14,6 +14,7 @@
 #include <vector>
 
 #include "engine.cuh"
+#include "tengine.cuh"
 
 using namespace slosim;
 
@@ -70,8 +71,8 @@ struct Arena {
 // results of sequential calls.
 constexpr int kMaxDevices = 64;
 struct DevState {
-    Arena ws, tabs, work, snap, io;
-    int sms = 0, blocks_per_sm = 0;
+    Arena ws, tabs, work, snap, io, lws, defer;
+    int sms = 0, blocks_per_sm = 0, lane_blocks_per_sm = 0;
     cudaEvent_t done = nullptr;
 };
 DevState g_dev[kMaxDevices];
@@ -92,6 +93,12 @@ int launch_geometry(DevState& ds, int dev, int64_t n_instances, int* grid) {
         CK(cudaDeviceGetAttribute(&ds.sms, cudaDevAttrMultiProcessorCount, dev));
         CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&ds.blocks_per_sm, sim_kernel, 128, 0));
         if (ds.blocks_per_sm < 1) ds.blocks_per_sm = 1;
+        CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&ds.lane_blocks_per_sm, lane::lane_kernel, 128, 0));
+        if (ds.lane_blocks_per_sm < 1) ds.lane_blocks_per_sm = 1;
+        if (const char* e = getenv("SLOSIM_LANE_BLOCKS_PER_SM")) {
+            int v = atoi(e);
+            if (v >= 1 && v < ds.lane_blocks_per_sm) ds.lane_blocks_per_sm = v;
+        }
         // experiment knob: fewer resident blocks per SM (occupancy studies)
         if (const char* e = getenv("SLOSIM_BLOCKS_PER_SM")) {
             int v = atoi(e);
@@ -166,7 +173,34 @@ extern "C" int slosim_run_batch(const slosim_batch_t* b, void* stream) {
     cx.B.max_requests = cap;
     cx.sched_tab = sched;
     cx.frozen_tab = frozen;
+    cx.dyn_n = nullptr;
     const bool force_lat = getenv("SLOSIM_FORCE_LATENCY_ENGINE") != nullptr;  // experiment knob
+    const bool full = (b->flags & (SLOSIM_F_ROWS | SLOSIM_F_EXPORT_LUT)) || b->trace_buf;
+    // Lane engine (tengine.cuh, one instance per thread) for throughput batches; the instances it
+    // does not cover are appended to a deferred list that the warp engine then runs in the same stream.
+    const bool lane_path = !full && !force_lat && !getenv("SLOSIM_NO_LANE_ENGINE") &&
+                           (b->n_instances > (int64_t)ds.sms * 4 || getenv("SLOSIM_FORCE_LANE_ENGINE"));
+    if (lane_path) {
+        int64_t lblocks = std::min<int64_t>((b->n_instances + 127) / 128, (int64_t)ds.sms * ds.lane_blocks_per_sm);
+        size_t lstride = lane::lws_bytes(cap, LUT_CELLS);
+        CK(ds.lws.reserve(lstride * (size_t)lblocks * 4, ds.done));
+        CK(ds.defer.reserve(sizeof(int64_t) * (size_t)b->n_instances + 256, ds.done));
+        unsigned long long* ctr = (unsigned long long*)ds.work.ptr;  // [0] lane work, [1] deferred count, [2] warp work
+        CK(cudaMemsetAsync(ctr, 0, 24, st));
+        lane::LCtx lc;
+        lc.B = cx.B;
+        lc.sched_tab = sched;
+        lc.deferred = (int64_t*)ds.defer.ptr;
+        lc.n_deferred = ctr + 1;
+        lane::lane_kernel<<<(int)lblocks, 128, 0, st>>>(lc, (char*)ds.lws.ptr, cap, LUT_CELLS, ctr);
+        CK(cudaGetLastError());
+        cx.B.order = (const int64_t*)ds.defer.ptr;
+        cx.dyn_n = ctr + 1;
+        sim_kernel<<<grid, 128, 0, st>>>(cx, (char*)ds.ws.ptr, stride, cap, ctr + 2);
+        CK(cudaGetLastError());
+        CK(cudaEventRecord(ds.done, st));
+        return SLOSIM_OK;
+    }
     if ((b->n_instances <= (int64_t)ds.sms * 4 || force_lat) && !getenv("SLOSIM_NO_LATENCY_ENGINE")) {
         // at most one 4-warp block per SM: the spill-free latency build (engine_lat.cu)
         CK(slosim_launch_latency_engine(grid, &cx, (char*)ds.ws.ptr, stride, cap, (unsigned long long*)ds.work.ptr,

@@ -405,6 +405,7 @@ struct Ctx {
     slosim_batch_t B;  // by value: lives in the kernel parameter (constant) bank
     const LutMem* sched_tab;
     const LutMem* frozen_tab;
+    const unsigned long long* dyn_n;  // non-null: the instance count is *dyn_n (instances deferred by the lane engine)
 };
 
 __device__ __forceinline__ int64_t arrival_of(const int64_t* Tarr, double fac, int p) {
@@ -1561,6 +1562,9 @@ __device__ SIM_INLINE void simulate(const Ctx& cx, int64_t ii, const WS& w, int 
             }
             if (FULL) S.T.used += 5 + nmem;
             dc_end = SLOSIM_INF64;
+            // no step runs now: an admission that switches to memory mode before the next decode
+            // start must not carry this batch's membership into the flag bits (to_memory_mode)
+            dc_mask = 0;
         }
 
         PROF_MARK(1);
@@ -1690,7 +1694,8 @@ __global__ void __launch_bounds__(128, SLOSIM_MIN_BLOCKS)
     const int lane = threadIdx.x & 31;
     const int64_t gw = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     WS w = make_ws(ws_base + (size_t)gw * ws_stride, cap);
-    const int64_t N = cx.B.n_instances;
+    const int64_t N = cx.dyn_n ? (int64_t)*cx.dyn_n : cx.B.n_instances;
+    const int64_t N_ids = cx.B.n_instances;  // instance ids range over the whole batch
     const bool full = (cx.B.flags & (SLOSIM_F_ROWS | SLOSIM_F_EXPORT_LUT)) || cx.B.trace_buf;
     for (;;) {
         unsigned long long k = 0;
@@ -1698,7 +1703,7 @@ __global__ void __launch_bounds__(128, SLOSIM_MIN_BLOCKS)
         k = __shfl_sync(FULLMASK, k, 0);
         if ((int64_t)k >= N) break;
         const int64_t ii = cx.B.order ? cx.B.order[k] : (int64_t)k;
-        if (ii < 0 || ii >= N) continue;  // not a permutation entry: skipped (C-ABI contract)
+        if (ii < 0 || ii >= N_ids) continue;  // not a permutation entry: skipped (C-ABI contract)
         const slosim_instance_t* I = cx.B.instances + ii;
         const bool kairos = I->decode_policy == SLOSIM_DECODE_KAIROS_SLACK;
         const bool pid_ok = I->profile_id >= 0 && I->profile_id < cx.B.n_profiles;

@@ -10,6 +10,7 @@
 // own namespace so its out-of-line device functions do not collide with the
 // throughput build's (capi.cu); the kernel context has the same layout.
 #include <cuda_runtime.h>
+#include <stdio.h>
 #include <string.h>
 
 #define SLOSIM_MIN_BLOCKS 1

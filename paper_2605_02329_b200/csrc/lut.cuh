@@ -310,6 +310,7 @@ __device__ __forceinline__ double geval_p(const LutMem* L, const Geo& g, const R
     return xadd(v1, xmul(xmul(xsub(v2, v1), (double)rp.num), rp.inv));
 }
 
+#ifdef __CUDACC__
 __device__ __forceinline__ void st_if(bool p, double* a, double v) {
     asm volatile("{\n\t.reg .pred q;\n\tsetp.ne.u32 q, %0, 0;\n\t@q st.f64 [%1], %2;\n\t}" ::"r"((unsigned)p), "l"(a),
                  "d"(v) : "memory");
@@ -318,6 +319,10 @@ __device__ __forceinline__ void st_if(bool p, int32_t* a, int32_t v) {
     asm volatile("{\n\t.reg .pred q;\n\tsetp.ne.u32 q, %0, 0;\n\t@q st.s32 [%1], %2;\n\t}" ::"r"((unsigned)p), "l"(a),
                  "r"(v) : "memory");
 }
+#else  // host test harness (tools/lane_host): plain predicated stores
+inline void st_if(bool p, double* a, double v) { if (p) *a = v; }
+inline void st_if(bool p, int32_t* a, int32_t v) { if (p) *a = v; }
+#endif
 
 // DecodeStepLUT.update (costmodel.py:118-128) on a full power-of-two grid:
 // lane 0 writes the cell, lane 1 the slope out of it, lane 2 the slope into it.

@@ -200,3 +200,22 @@ def test_gpu_equals_oracle_on_config5_stride_sample(lib):
     assert len(set(sw.coords["trace"].tolist())) == 252
     assert len(set(sw.coords["pair"].tolist())) == 4 and len(set(sw.coords["rate"].tolist())) == 64
     _summaries_equal(got, ref.packed.summaries)
+
+
+@pytest.mark.parametrize("env", ["SLOSIM_FORCE_LATENCY_ENGINE", "SLOSIM_NO_LATENCY_ENGINE"])
+def test_regression_memory_mode_switch_after_partial_batch(lib, env, monkeypatch):
+    """Config-5 instance 130145 (fcfs + kairos-slack, rate 2.55, SLO x2.25): a slack-guided partial
+    batch completes, then admissions at the same instant lift the active set above 32 (register ->
+    memory mode) before the next decode start.  The completed batch's membership used to leak into
+    the memory-mode flag bits, so the next partial batch decoded 28 extra requests.  Found by the
+    full config-5 cross-check of the warp engine against the lane engine (tools/xcheck.py)."""
+    from oracle import oracle
+    from paper_2605_02329_b200.batch import config5, run_batch
+
+    monkeypatch.setenv(env, "1")
+    monkeypatch.setenv("SLOSIM_NO_LANE_ENGINE", "1")
+    sel = np.array([130145, 130144, 130146, 130147])
+    got = run_batch(config5(select=sel).packed).copy()
+    ref = config5(select=sel, synth=oracle.synth)
+    oracle.run_batch(ref.packed, threads=4)
+    _summaries_equal(got, ref.packed.summaries)
