@@ -3,8 +3,9 @@
 Workload (BASELINE.json metric "simulated requests/sec (1/2/4/8 B200)"): SURVEY
 Appendix B config 5 — 256 trace seeds x 64 arrival rates x 16 SLO scales x 4
 policy pairs = 1,048,576 independent instances of 1k requests, sharded across
-GPUs.  One *step* is one slice of 16,384 instances (16.4M simulated requests)
-per GPU; rank r takes slices s*G + r (weak scaling).  The timed region is K
+GPUs.  One *step* is one slice of 131,072 instances (131M simulated requests)
+per GPU, so the default 3 warm-up + 5 timed steps cover all of config 5 once;
+rank r takes slices s*G + r (weak scaling).  The timed region is K
 steps (kernel launches on device-resident inputs, L2 flushed between steps by
 a 256 MiB write) followed by the final exchange: the per-(pair, rate, SLO)
 e2e-attainment histogram build, an NCCL int64 all-reduce and an all-gather of
@@ -48,7 +49,7 @@ import numpy as np
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
-SLICE = 16384
+SLICE = 131072
 # instances of each SURVEY Appendix B config and its (pairs, SLO scales, rates) histogram grid
 N_TOTAL = {"config1": 12, "config2": 2, "config3": 3072, "config4": 2048, "config5": 256 * 64 * 16 * 4}
 GRID = {"config1": (2, 1, 6), "config2": (2, 1, 1), "config3": (3, 16, 64), "config4": (2, 1, 1),
@@ -66,7 +67,7 @@ def parse(argv=None):
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--workload", default="config5", choices=sorted(N_TOTAL))
     ap.add_argument("--slice", type=int, default=SLICE, help="config5 instances per step per GPU")
-    ap.add_argument("--cpu-sample-s", type=float, default=12.0, help="target seconds of oracle work")
+    ap.add_argument("--cpu-sample-s", type=float, default=10.0, help="target seconds of oracle work")
     ap.add_argument("--pyref-sample", type=int, default=-1,
                     help="instances of the Python reference baseline (-1: workload default, 0: off)")
     ap.add_argument("--no-e2e", action="store_true")
@@ -542,7 +543,9 @@ def main(argv=None):
             "parity": parity,
             "exchange": exchange,
             "clocks": clocks,
-            "gpu_launches": 3 * len(timed),
+            # per step: build_profile_tables, lane_kernel, sim_kernel (instances the lane engine defers;
+            # none on config 5), and k_histogram in the exchange
+            "gpu_launches": 4 * len(timed),
             "kernel_ms_per_step": step_ms,
             "mean_kernel_ms_max_over_ranks": mean_ms_max,
         }

@@ -9,7 +9,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 OUT = os.path.join(HERE, "libslosim_b200.so")
 SOURCES = ["capi.cu", "engine_lat.cu"]
-HEADERS = ["engine.cuh", "lut.cuh", "numerics.cuh", os.path.join("..", "..", "include", "slosim_b200.h")]
+HEADERS = ["engine.cuh", "tengine.cuh", "warpops.cuh", "lut.cuh", "numerics.cuh", os.path.join("..", "..", "include", "slosim_b200.h")]
 
 NVCC_FLAGS = [
     "-gencode", "arch=compute_100a,code=sm_100a",

@@ -178,8 +178,12 @@ extern "C" int slosim_run_batch(const slosim_batch_t* b, void* stream) {
     const bool full = (b->flags & (SLOSIM_F_ROWS | SLOSIM_F_EXPORT_LUT)) || b->trace_buf;
     // Lane engine (tengine.cuh, one instance per thread) for throughput batches; the instances it
     // does not cover are appended to a deferred list that the warp engine then runs in the same stream.
+    // One instance per thread pays off once the batch fills every lane slot of the GPU at least
+    // once (sms x resident blocks x 128 lanes, 37,888 on a B200); smaller batches run faster as
+    // one instance per warp.
+    const int64_t lane_slots = (int64_t)ds.sms * ds.lane_blocks_per_sm * 128;
     const bool lane_path = !full && !force_lat && !getenv("SLOSIM_NO_LANE_ENGINE") &&
-                           (b->n_instances > (int64_t)ds.sms * 4 || getenv("SLOSIM_FORCE_LANE_ENGINE"));
+                           (b->n_instances >= lane_slots || getenv("SLOSIM_FORCE_LANE_ENGINE"));
     if (lane_path) {
         int64_t lblocks = std::min<int64_t>((b->n_instances + 127) / 128, (int64_t)ds.sms * ds.lane_blocks_per_sm);
         size_t lstride = lane::lws_bytes(cap, LUT_CELLS);

@@ -50,3 +50,6 @@ static inline unsigned __activemask() { return 1u; }
 static inline unsigned long long atomicAdd(unsigned long long* p, unsigned long long v) {
     unsigned long long o = *p; *p += v; return o;
 }
+template <class T> static inline T __shfl_up_sync(unsigned, T, int) { hc_no_warp(); }
+static inline int __reduce_min_sync(unsigned, int) { hc_no_warp(); }
+static inline int __all_sync(unsigned, int) { hc_no_warp(); }

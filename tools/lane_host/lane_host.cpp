@@ -8,11 +8,11 @@
 
 // decode-step log of the last instance run (debugging aid: t_end, duration, bsz, max_seq per step)
 static std::vector<int64_t> g_log;
-#define LANE_HOOK_DECODE(H, w)                                                                    \
+#define LANE_HOOK_DECODE(S, w)                                                                    \
     do {                                                                                          \
-        g_log.push_back((H).dc_end); g_log.push_back((H).dc_dur); g_log.push_back((H).dc_bsz);    \
-        g_log.push_back((H).dc_max); g_log.push_back((H).an);                                     \
-        for (int q = 0; q < (H).an; q++) { g_log.push_back((w).i32(A_POS)[q]); g_log.push_back((w).i32(A_SEQ)[q]); } \
+        g_log.push_back((S).dc_end); g_log.push_back((S).dc_dur); g_log.push_back((S).dc_bsz);    \
+        g_log.push_back((S).dc_max); g_log.push_back((S).an);                                     \
+        for (int q = 0; q < (S).an; q++) { g_log.push_back((w).a32(A_POS)[q]); g_log.push_back((w).a32(A_SEQ)[q]); } \
     } while (0)
 
 #include "../../paper_2605_02329_b200/csrc/tengine.cuh"
@@ -68,11 +68,9 @@ extern "C" int lane_host_run_batch(const slosim_batch_t* B) {
             continue;
         }
         St S;
-        Hot H;
         g_log.clear();
         if (!linit(S, cx, w, ii)) continue;
-        lhot_init(H, S, cx);
-        while (lstep(H, S, cx, w)) {
+        while (lstep(S, cx, w)) {
         }
     }
     return 0;
