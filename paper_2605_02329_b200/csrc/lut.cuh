@@ -469,8 +469,13 @@ __device__ __forceinline__ bool gt_line_make(int n, const int64_t* bx, const dou
     return true;
 }
 __device__ __forceinline__ double gt_line_eval(const GtLine& k, int64_t bsz, int64_t seq) {
+#ifdef SLOSIM_GT_BRANCH
+    double base = seq <= k.x0 ? k.y0 : k.y1;
+    if (seq > k.x0 && seq < k.x1) base = xadd(k.y0, xdiv(xmul(k.dy, (double)(seq - k.x0)), k.dx));
+#else
     const double mid = xadd(k.y0, xdiv(xmul(k.dy, (double)(seq - k.x0)), k.dx));
     const double base = seq <= k.x0 ? k.y0 : (seq >= k.x1 ? k.y1 : mid);
+#endif
     return xmul(base, xadd(1.0, xmul(k.gamma, (double)(bsz - 1))));
 }
 
