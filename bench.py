@@ -494,7 +494,8 @@ def main(argv=None):
                 "hist_total": int(h_host.sum()), "hist_sha16": hashlib.sha256(h_host.tobytes()).hexdigest()[:16],
                 "rows_sha16": hashlib.sha256(g_rows.tobytes()).hexdigest()[:16]}
 
-    # roofline of the dominant kernel (sim_kernel): algorithmic bytes / mean launch duration
+    # roofline of the dominant kernel (lane_kernel; sim_kernel below one wave of lanes): algorithmic bytes /
+    # mean launch duration
     peak, peak_kind = load_peaks()
     abytes = alg_bytes(summ) / len(timed)
     mean_ms = float(np.mean(step_ms))

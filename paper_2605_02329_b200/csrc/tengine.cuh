@@ -179,9 +179,8 @@ struct St {
     int64_t ii;
     int64_t off;  // trace offset
     const slosim_profile_t* P;
-    double fac, tpt;
-    int64_t ttft_slo, tpot_slo, kv_cap, tr_base;
-    int n, budget;
+    int64_t ttft_slo, tpot_slo;
+    int n;
     int8_t ppol, dpol;
     bool use_lut, gline;
     LGeo g;
@@ -197,9 +196,13 @@ struct St {
     uint64_t D;
 };
 
+// Rarely used per-instance parameters are read from the descriptor (not kept in registers).
+__device__ __forceinline__ const slosim_instance_t& linst(const LCtx& cx, const St& S) { return cx.B.instances[S.ii]; }
+
 __device__ __forceinline__ int64_t larrival(const LCtx& cx, const St& S, int p) {
     const int64_t a = cx.B.traces.arrival_us[S.off + p];
-    return S.fac > 0 ? rint_i64(xmul((double)a, S.fac)) : a;
+    const double fac = linst(cx, S).rescale_factor;
+    return fac > 0 ? rint_i64(xmul((double)a, fac)) : a;
 }
 
 __device__ __forceinline__ bool linstance_ok(const slosim_batch_t* B, const slosim_instance_t* I, const LutMem* tabs) {
@@ -236,13 +239,8 @@ __device__ __forceinline__ bool linit(St& S, const LCtx& cx, const LWs& w, int64
     const int pid = I->profile_id;
     S.P = B->profiles + pid;
     S.off = I->trace_offset;
-    S.fac = I->rescale_factor;
     S.ttft_slo = I->ttft_slo_us;
     S.tpot_slo = I->tpot_slo_us;
-    S.kv_cap = I->kv_capacity_tokens;
-    S.tr_base = I->transfer_base_us;
-    S.tpt = I->transfer_per_token_us;
-    S.budget = I->chunk_budget;
     S.ppol = I->prefill_policy;
     S.dpol = I->decode_policy;
     const LutMem* ST = cx.sched_tab + pid;
@@ -254,7 +252,7 @@ __device__ __forceinline__ bool linit(St& S, const LCtx& cx, const LWs& w, int64
         const int64_t need = (int64_t)Tinp[p] + Tout[p];
         worst = need > worst ? need : worst;
     }
-    if (worst > S.kv_cap || ST->rowmask == 0) {
+    if (worst > I->kv_capacity_tokens || ST->rowmask == 0) {
         lwrite_status(B->summaries + ii, S.n, SLOSIM_ECONFIG);
         return false;
     }
@@ -378,7 +376,8 @@ __device__ __forceinline__ void lrare(St& S, const LCtx& cx, const LWs& w, int64
             h = dstep(h, ((uint64_t)(uint32_t)pos << 32) | (uint32_t)take);
             if (rem == 0) {  // completed: leaves the queue, KV transfer in batch order
                 ncomp++;
-                const int64_t delay = S.tr_base + rint_i64(xmul((double)QI[qi], S.tpt));
+                const slosim_instance_t& I = linst(cx, S);
+                const int64_t delay = I.transfer_base_us + rint_i64(xmul((double)QI[qi], I.transfer_per_token_us));
                 if (delay == 0) {
                     lpending_insert(S, w, t, Tidr[pos], t, pos);
                 } else {
@@ -419,11 +418,12 @@ __device__ __forceinline__ void ladmit(St& S, const LCtx& cx, const LWs& w) {
     const auto AP = w.a32(A_POS), AS = w.a32(A_SEQ), AI = w.a32(A_IDR), AO = w.a32(A_OUT), AN = w.a32(A_INP),
                AM = w.a32(A_MISS), AF = w.a32(A_FLAG);
     const auto AT = w.a64(A_TF);
+    const int64_t kv_cap = linst(cx, S).kv_capacity_tokens;
     while (S.pt > S.ph) {
         const int32_t pos = PP[S.ph];
         const int32_t outl = Tout[pos], inp = Tinp[pos];
         const int64_t need = (int64_t)inp + outl;
-        if (S.kv + need > S.kv_cap) break;  // head-of-line blocking
+        if (S.kv + need > kv_cap) break;  // head-of-line blocking
         const int64_t ttr = PR[S.ph];
         const int32_t idr = PI[S.ph];
         S.ph++;
@@ -453,7 +453,7 @@ __device__ __forceinline__ void ladmit(St& S, const LCtx& cx, const LWs& w) {
 
 // ---- start a prefill step on this lane alone (engine.py:307-325, prefill_sched.py:93-145); the
 // host test harness uses it, the kernel starts prefill steps cooperatively (coop_prefill_start).
-__device__ __forceinline__ void lprefill_start(St& S, const LWs& w, int64_t t) {
+__device__ __forceinline__ void lprefill_start(St& S, const LCtx& cx, const LWs& w, int64_t t) {
     const auto QR = w.r32(Q_REM), QF = w.r32(Q_FULL), QI = w.r32(Q_INP);
     const auto QA = w.r64(Q_ARR);
     const auto QK = w.r64f(Q_SCORE);
@@ -462,7 +462,7 @@ __device__ __forceinline__ void lprefill_start(St& S, const LWs& w, int64_t t) {
     S.v_pre += qlen;
     S.max_q = qlen > S.max_q ? qlen : S.max_q;
     int k = 0;
-    int64_t left = S.budget;
+    int64_t left = linst(cx, S).chunk_budget;
     if (S.ppol == SLOSIM_PREFILL_FCFS) {
         for (int qi = S.qh; qi < S.qt && left > 0; qi++) {
             const int64_t rem = QR[qi];
@@ -739,7 +739,7 @@ __device__ __forceinline__ bool lstep(St& S, const LCtx& cx, const LWs& w) {
     int64_t t;
     bool need_pf;
     if (!lstep_a(S, cx, w, t, need_pf)) return false;
-    if (need_pf) lprefill_start(S, w, t);
+    if (need_pf) lprefill_start(S, cx, w, t);
     lstep_c(S, w, t);
     return true;
 }
@@ -784,7 +784,7 @@ __global__ void __launch_bounds__(128, SLOSIM_LANE_MIN_BLOCKS)
         // prefill starts: FCFS packs a prefix of the queue, cheap on the lane itself; the urgency and
         // SJF policies order the whole queue, so one lane's queue at a time, all lanes cooperating
         if (need_pf && S.ppol == SLOSIM_PREFILL_FCFS) {
-            lprefill_start(S, w, t);
+            lprefill_start(S, cx, w, t);
             need_pf = false;
         }
         __syncwarp();
@@ -792,7 +792,7 @@ __global__ void __launch_bounds__(128, SLOSIM_LANE_MIN_BLOCKS)
             const int L = __ffs((int)m) - 1;
             const PfOut r = coop_prefill_start(
                 w.for_lane(L).ws(), __shfl_sync(FULLMASK, (int)S.ppol, L), __shfl_sync(FULLMASK, S.qh, L),
-                __shfl_sync(FULLMASK, S.qt, L), __shfl_sync(FULLMASK, (int64_t)S.budget, L),
+                __shfl_sync(FULLMASK, S.qt, L), __shfl_sync(FULLMASK, (int64_t)linst(cx, S).chunk_budget, L),
                 __shfl_sync(FULLMASK, t, L), __shfl_sync(FULLMASK, S.est_tok, L),
                 __shfl_sync(FULLMASK, S.est_busy, L), __shfl_sync(FULLMASK, S.ttft_slo, L),
                 (const slosim_profile_t*)__shfl_sync(FULLMASK, (unsigned long long)S.P, L), lane);
