@@ -757,6 +757,7 @@ __global__ void __launch_bounds__(128, SLOSIM_LANE_MIN_BLOCKS)
     const LWs w{ws_base + (size_t)gw * warp_bytes, (size_t)(cap > 0 ? cap : 1), cells, lane};
     const int64_t N = cx.B.n_instances;
     St S;
+    S.ii = 0;
     bool live = false, done = false;  // live: an instance in progress; done: the work queue is drained
     for (;;) {
         if (!live && !done) {
@@ -787,12 +788,13 @@ __global__ void __launch_bounds__(128, SLOSIM_LANE_MIN_BLOCKS)
             lprefill_start(S, cx, w, t);
             need_pf = false;
         }
+        const int64_t budget = need_pf ? (int64_t)linst(cx, S).chunk_budget : 0;  // lanes with a queue only
         __syncwarp();
         for (unsigned m = __ballot_sync(FULLMASK, need_pf); m; m &= m - 1) {
             const int L = __ffs((int)m) - 1;
             const PfOut r = coop_prefill_start(
                 w.for_lane(L).ws(), __shfl_sync(FULLMASK, (int)S.ppol, L), __shfl_sync(FULLMASK, S.qh, L),
-                __shfl_sync(FULLMASK, S.qt, L), __shfl_sync(FULLMASK, (int64_t)linst(cx, S).chunk_budget, L),
+                __shfl_sync(FULLMASK, S.qt, L), __shfl_sync(FULLMASK, budget, L),
                 __shfl_sync(FULLMASK, t, L), __shfl_sync(FULLMASK, S.est_tok, L),
                 __shfl_sync(FULLMASK, S.est_busy, L), __shfl_sync(FULLMASK, S.ttft_slo, L),
                 (const slosim_profile_t*)__shfl_sync(FULLMASK, (unsigned long long)S.P, L), lane);

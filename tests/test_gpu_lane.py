@@ -51,3 +51,17 @@ def test_mixed_batch_defers_out_of_scope_instances_to_the_warp_engine(monkeypatc
     got = run_batch(packed)
     bad = {i: m for i, c in enumerate(cases) if (m := summary_mismatches(got[i], c["summary"]))}
     assert not bad, f"{len(bad)} cases differ: {dict(list(bad.items())[:5])}"
+
+
+def test_lane_engine_on_batches_smaller_than_a_warp(monkeypatch):
+    """Forced onto a 12-instance batch (config 1), most lanes of the grid never hold an instance:
+    they must take part in the cooperative prefill starts without touching any descriptor."""
+    from helpers import load_golden, summary_mismatches
+
+    from paper_2605_02329_b200.batch import config1, run_batch
+
+    monkeypatch.setenv("SLOSIM_FORCE_LANE_ENGINE", "1")
+    got = run_batch(config1().packed)
+    golden = load_golden()["config1"]
+    for i in range(12):
+        assert summary_mismatches(got[i], golden[i]["summary"]) == [], i
