@@ -101,3 +101,21 @@ def test_random_instances_equal_oracle(rows):
     if rows:
         for k, v in ref.rows.items():
             assert np.array_equal(packed.rows[k], v, equal_nan=True), k
+
+
+def test_random_instances_equal_oracle_lane_engine(monkeypatch):
+    """The same random sweep forced through the lane engine (one instance per thread); instances outside
+    its scope (table grids, partially populated LUTs, noise) are deferred to the warp engine in the same
+    launch.  Bursts of up to ~400 requests exercise active sets beyond the 64-entry batch mask."""
+    from oracle import oracle
+    from paper_2605_02329_b200.batch import run_batch
+
+    monkeypatch.setenv("SLOSIM_FORCE_LANE_ENGINE", "1")
+    got = run_batch(_batch()).copy()
+    ref = _batch(synth=oracle.synth)
+    oracle.run_batch(ref, threads=8)
+    want = ref.summaries
+    for k in [x for x in want.dtype.names if x != "sim_cycles"]:
+        a, b = got[k], want[k]
+        eq = np.array_equal(a, b, equal_nan=True) if a.dtype.kind == "f" else np.array_equal(a, b)
+        assert eq, (k, int(np.flatnonzero(a != b)[0]) if not eq and a.dtype.kind != "f" else None)

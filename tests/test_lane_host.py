@@ -71,3 +71,27 @@ def test_lane_engine_matches_oracle_on_config5_and_config3_samples(lane):
             a, b = got[f], want[f]
             eq = np.array_equal(a, b, equal_nan=True) if a.dtype.kind == "f" else np.array_equal(a, b)
             assert eq, (name, f)
+
+
+def test_lane_engine_matches_oracle_on_random_sweep(lane):
+    """The GPU fuzz sweep's random instances (tests/test_gpu_fuzz.py) that the lane engine covers:
+    bursts beyond 64 concurrent decodes, KV gating, transfer delays, prefix hits, every policy pair."""
+    import importlib.util
+
+    from oracle import oracle
+
+    spec = importlib.util.spec_from_file_location("fuzz", os.path.join(ROOT, "tests", "test_gpu_fuzz.py"))
+    fuzz = importlib.util.module_from_spec(spec)
+    spec.loader.exec_module(fuzz)
+    packed = fuzz._batch(synth=oracle.synth, n_inst=400)
+    got = _run(lane, packed).copy()
+    ref = fuzz._batch(synth=oracle.synth, n_inst=400)
+    oracle.run_batch(ref, threads=os.cpu_count() or 4)
+    want = ref.summaries
+    cov = got["status"] != -99
+    assert cov.sum() > 100
+    assert int(want[cov]["max_active"].max()) > 64
+    for f in [x for x in want.dtype.names if x != "sim_cycles"]:
+        a, b = got[f][cov], want[f][cov]
+        eq = np.array_equal(a, b, equal_nan=True) if a.dtype.kind == "f" else np.array_equal(a, b)
+        assert eq, f
