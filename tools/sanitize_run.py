@@ -1,5 +1,6 @@
 """Small engine workload for compute-sanitizer: config-1 instances (both pairs) in the throughput and the
-row/trace specialisations, a slice of the fuzz sweep (memory mode, table LUTs, noise) and the snapshot kernels."""
+row/trace specialisations, a slice of the fuzz sweep (memory mode, table LUTs, noise), a traced Simulation,
+and the same small batches forced through the lane engine."""
 import os
 import sys
 
@@ -24,4 +25,11 @@ wl = gen_longtail(LongTailSpec(n_requests=200))
 sim = slosim.Simulation(slosim.ClusterConfig(prefill_policy="kairos-urgency", decode_policy="kairos-slack"), wl,
                         collect_events=True)
 sim.run()
+# the lane engine (one instance per thread), forced onto small batches: config 1 and a fuzz slice
+# (cooperative prefill starts, deferral of out-of-scope instances to the warp engine)
+os.environ["SLOSIM_FORCE_LANE_ENGINE"] = "1"
+s = run_batch(config1().packed)
+assert np.all(s["status"] == 0)
+run_batch(F._batch(flags=0, n_inst=N, seed=7))
+del os.environ["SLOSIM_FORCE_LANE_ENGINE"]
 print("sanitize_run ok")
