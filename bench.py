@@ -180,10 +180,43 @@ class ClockSampler:
 
 
 # ------------------------------------------------------------- workloads ---
-def build_workload(name, synth=None, select=None):
+def build_workload(name, synth=None, select=None, gen="host"):
     from paper_2605_02329_b200 import batch as B
 
-    return B.CONFIGS[name](select=select, synth=synth)
+    return B.CONFIGS[name](select=select, synth=synth, gen=gen)
+
+
+def workload_specs(name):
+    from paper_2605_02329_b200.workload import LongTailSpec
+
+    if name in ("config1", "config3"):
+        return [LongTailSpec()]
+    if name == "config2":
+        return [LongTailSpec(n_requests=100_000, seed=2024, qps=1.0)]
+    if name == "config4":
+        return [LongTailSpec(n_requests=20_000, seed=s, qps=4.0) for s in range(256)]
+    return [LongTailSpec(seed=s) for s in range(256)]
+
+
+def trace_generation(name):
+    """The workload's traces generated on the device (slosim_gen_longtail) and by numpy on
+    the host (the reference's generator): both timed, compared field by field."""
+    from paper_2605_02329_b200.workload import longtail_arrays, longtail_arrays_device
+
+    specs = workload_specs(name)
+    longtail_arrays_device(specs[:1])  # context and module load outside the timing
+    t0 = time.perf_counter()
+    dev = longtail_arrays_device(specs)
+    dev_s = time.perf_counter() - t0
+    t0 = time.perf_counter()
+    host = [longtail_arrays(s) for s in specs]
+    host_s = time.perf_counter() - t0
+    same = all(np.array_equal(getattr(a, k), getattr(b, k)) for a, b in zip(dev, host)
+               for k in ("arrival_us", "input_len", "output_len", "prefix_hit_len", "id_rank"))
+    return {"generator": "slosim_gen_longtail (device, one thread per trace; host copies included)",
+            "traces": len(specs), "requests": int(sum(s.n_requests for s in specs)),
+            "device_ms": round(dev_s * 1e3, 2), "host_numpy_ms": round(host_s * 1e3, 2),
+            "identical_to_numpy": bool(same)}
 
 
 def workload_meta(name, slice_n):
@@ -415,8 +448,12 @@ def main(argv=None):
     n_total = N_TOTAL[args.workload]
     slice_n = slice_size(args)
     n_slices = max(1, n_total // slice_n)
+    traces_info = trace_generation(args.workload)
+    if not traces_info["identical_to_numpy"]:
+        print("bench.py: device-generated traces differ from numpy's", file=sys.stderr)
+        return 3
     t_pack = time.perf_counter()
-    sw = build_workload(args.workload)
+    sw = build_workload(args.workload, gen="device")
     pack_s = time.perf_counter() - t_pack
     db = DeviceBatch(sw.packed)
     n_pairs, n_slo, n_rates = GRID[args.workload]
@@ -526,7 +563,8 @@ def main(argv=None):
             "metric": metric_name(), "value": value, "unit": "simulated requests/s", "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": elapsed_ms / args.steps,
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "int64+f64",
-            "data": "synthetic (reference LongTailSpec generator, host numpy; identical traces on CPU and GPU)",
+            "data": "synthetic (reference LongTailSpec generator restated on the device, slosim_gen_longtail; "
+                    "bit-identical to numpy's, checked every run; the CPU arms use numpy's)",
             "config": dict(workload_meta(args.workload, slice_n), parallelism=f"instances sharded over {world} GPU(s)"),
             "e2e": e2e,
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "peak_kind": peak_kind, "unit": "GB/s",
@@ -535,10 +573,11 @@ def main(argv=None):
                          "alg_bytes_per_launch": abytes, "mean_launch_ms": mean_ms,
                          "floor_bytes_per_launch": floor_bytes,
                          "issue_frac": (ncu_counters or {}).get("smsp__issue_active_pct", 0) / 100 or None,
-                         "issue_note": "fraction of SMSP issue slots used by sim_kernel (ncu smsp__issue_active of "
+                         "issue_note": "fraction of SMSP issue slots used by lane_kernel (ncu smsp__issue_active of "
                                        "the committed capture): the path is issue/latency bound, not HBM bound",
                          "ncu_counters": ncu_counters},
             "host_pack_s": round(pack_s, 2),
+            "trace_generation": traces_info,
             "cpu_baseline": cpu,
             "cpu_baseline_python": pyref,
             "parity": parity,

@@ -29,6 +29,7 @@ extern "C" {
 #define SLOSIM_ECONFIG 3
 #define SLOSIM_ECUDA 4
 #define SLOSIM_ENOMEM 5
+#define SLOSIM_ERANGE 6  /* a generated value left the covered range (gen_longtail: token count > int32) */
 
 /* Grid limits of the decode step LUT (costmodel.py:26-27 default 9 x 32). */
 #define SLOSIM_MAX_BSZ_BUCKETS 16
@@ -273,6 +274,58 @@ int slosim_histogram(int64_t n, const slosim_summary_t* d_summaries, const int32
  * at run time; returns SLOSIM_ECUDA with slosim_last_error() if it is missing. */
 int slosim_exchange(void* nccl_comm, const slosim_summary_t* d_mine, int64_t n_mine, slosim_summary_t* d_all,
                     int64_t* d_hist, int64_t n_hist, void* stream);
+
+/* ------------------------------------------------ workload generation (§8(f)4)
+ * LongTailSpec (workload.py:52-85): the fields of the reference dataclass, plus
+ * where the trace goes in the output trace table. */
+typedef struct slosim_longtail_spec {
+    double qps;
+    int64_t n_requests;
+    double short_len_log_mean;
+    double short_len_log_sigma;
+    double p_long;
+    int64_t long_len_min;
+    int64_t long_len_max;
+    double out_len_log_mean;
+    double out_len_log_sigma;
+    uint64_t seed;      /* default_rng(seed); 0 <= seed < 2^64 */
+    int64_t offset;     /* first request's position in the output arrays */
+} slosim_longtail_spec_t;
+
+/* Replaces gen_longtail (workload.py:88-112), batched over specs: trace i is written
+ * at [offset_i, offset_i + n_requests_i) of the output SoA, in (arrival, id) order,
+ * with prefix_hit_len = 0 and id_rank = position (ids r{k:0w} sort by position).
+ * The draws are numpy's (default_rng(seed): SeedSequence, PCG64, ziggurat
+ * exponential/normal, Lemire integers; glibc exp/log1p), so the trace is identical
+ * to the reference's.  d_status[i]: SLOSIM_OK, SLOSIM_EINVAL (spec fails
+ * LongTailSpec's checks, tail range >= 2^32 - 1, or out of the table) or
+ * SLOSIM_ERANGE.  DEVICE pointers, stream-ordered. */
+int slosim_gen_longtail(const slosim_longtail_spec_t* d_specs, int64_t n_specs, int64_t* d_arrival_us,
+                        int32_t* d_input_len, int32_t* d_output_len, int32_t* d_prefix_hit_len,
+                        int32_t* d_id_rank, int64_t n_total, int32_t* d_status, void* stream);
+
+/* Same with HOST pointers (copies in and out, synchronizes). */
+int slosim_gen_longtail_host(const slosim_longtail_spec_t* specs, int64_t n_specs, int64_t* arrival_us,
+                             int32_t* input_len, int32_t* output_len, int32_t* prefix_hit_len,
+                             int32_t* id_rank, int64_t n_total, int32_t* status);
+
+/* Test-level: n_per_seed draws of one Generator method for each default_rng(seed),
+ * computed on the device (HOST pointers; out[i * n_per_seed + k], f64 results as
+ * their bit patterns).  INTEGERS draws integers(p0, p1) (high exclusive, range below
+ * 2^32 - 1); EXPONENTIAL uses scale p0; LOGNORMAL mean p0, sigma p1. */
+#define SLOSIM_DRAW_RAW 0
+#define SLOSIM_DRAW_RANDOM 1
+#define SLOSIM_DRAW_STD_EXPONENTIAL 2
+#define SLOSIM_DRAW_EXPONENTIAL 3
+#define SLOSIM_DRAW_STD_NORMAL 4
+#define SLOSIM_DRAW_LOGNORMAL 5
+#define SLOSIM_DRAW_INTEGERS 6
+int slosim_rng_draws(int32_t kind, const uint64_t* seeds, int64_t n_seeds, int64_t n_per_seed, double p0,
+                     double p1, uint64_t* out, int32_t* status);
+
+/* Test-level: the device restatement of libm exp (fn 0) / log1p (fn 1) that the
+ * draws use, over x[n] (HOST pointers); ok[k] = 0 outside the restated domain. */
+int slosim_libm(int32_t fn, int64_t n, const double* x, double* y, uint8_t* ok);
 
 /* Library identity (ABI version, sm arch compiled for) and visible CUDA devices. */
 int slosim_abi_version(void);

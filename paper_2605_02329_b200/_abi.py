@@ -22,6 +22,9 @@ EINVAL = 2
 ECONFIG = 3
 ECUDA = 4
 ENOMEM = 5
+ERANGE = 6
+
+DRAW_RAW, DRAW_RANDOM, DRAW_STD_EXPONENTIAL, DRAW_EXPONENTIAL, DRAW_STD_NORMAL, DRAW_LOGNORMAL, DRAW_INTEGERS = range(7)
 
 PREFILL_IDS = {"fcfs": 0, "sjf": 1, "kairos-urgency": 2}
 DECODE_IDS = {"continuous": 0, "kairos-slack": 1}
@@ -91,6 +94,24 @@ class Traces(ctypes.Structure):
         ("prefix_hit_len", c_void_p),
         ("id_rank", c_void_p),
         ("n_total", c_int64),
+    ]
+
+
+class LongTailSpec(ctypes.Structure):
+    """slosim_longtail_spec_t: LongTailSpec (workload.py:52-85) + output offset."""
+
+    _fields_ = [
+        ("qps", c_double),
+        ("n_requests", c_int64),
+        ("short_len_log_mean", c_double),
+        ("short_len_log_sigma", c_double),
+        ("p_long", c_double),
+        ("long_len_min", c_int64),
+        ("long_len_max", c_int64),
+        ("out_len_log_mean", c_double),
+        ("out_len_log_sigma", c_double),
+        ("seed", c_uint64),
+        ("offset", c_int64),
     ]
 
 
@@ -227,6 +248,10 @@ def lib():
     L.slosim_request_metrics.argtypes = [c_int64, vp, vp, vp, vp, c_int64, c_int64, vp, vp, vp, vp, vp, vp]
     L.slosim_histogram.argtypes = [c_int64, vp, vp, c_int32, vp, vp]
     L.slosim_exchange.argtypes = [vp, vp, c_int64, vp, vp, c_int64, vp]
+    L.slosim_gen_longtail.argtypes = [vp, c_int64, vp, vp, vp, vp, vp, c_int64, vp, vp]
+    L.slosim_gen_longtail_host.argtypes = [vp, c_int64, vp, vp, vp, vp, vp, c_int64, vp]
+    L.slosim_rng_draws.argtypes = [c_int32, vp, c_int64, c_int64, c_double, c_double, vp, vp]
+    L.slosim_libm.argtypes = [c_int32, c_int64, vp, vp, vp]
     L.slosim_abi_version.restype = c_int
     L.slosim_last_error.restype = c_char_p
     L.slosim_build_info.restype = c_char_p
@@ -254,6 +279,10 @@ HEADER_SYMBOLS = [
     "slosim_prefill_batch_us",
     "slosim_request_metrics",
     "slosim_histogram",
+    "slosim_gen_longtail",
+    "slosim_gen_longtail_host",
+    "slosim_rng_draws",
+    "slosim_libm",
     "slosim_abi_version",
     "slosim_device_count",
     "slosim_build_info",

@@ -8,8 +8,8 @@ import subprocess
 HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 OUT = os.path.join(HERE, "libslosim_b200.so")
-SOURCES = ["capi.cu", "engine_lat.cu"]
-HEADERS = ["engine.cuh", "tengine.cuh", "warpops.cuh", "lut.cuh", "numerics.cuh", os.path.join("..", "..", "include", "slosim_b200.h")]
+SOURCES = ["capi.cu", "engine_lat.cu", "longtail.cu"]
+HEADERS = ["engine.cuh", "tengine.cuh", "warpops.cuh", "lut.cuh", "numerics.cuh", "rng.cuh", "rng_tables.h", os.path.join("..", "..", "include", "slosim_b200.h")]
 
 NVCC_FLAGS = [
     "-gencode", "arch=compute_100a,code=sm_100a",

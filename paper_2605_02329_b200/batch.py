@@ -20,7 +20,7 @@ import numpy as np
 from . import _abi
 from .config import ClusterConfig, CostProfile
 from .pack import PackedBatch, profile_struct
-from .workload import LongTailSpec, TraceArrays, longtail_arrays, rescale_factor
+from .workload import LongTailSpec, TraceArrays, longtail_arrays, longtail_arrays_device, rescale_factor
 
 PAIRS_2 = [("fcfs", "continuous"), ("kairos-urgency", "kairos-slack")]
 PAIRS_3 = [("fcfs", "continuous"), ("sjf", "continuous"), ("kairos-urgency", "kairos-slack")]
@@ -127,21 +127,31 @@ def _rescale_order_ok(tr: TraceArrays, factor: float) -> bool:
 
 
 # ----------------------------------------------------- SURVEY Appendix B ---
-def config1(**kw) -> Sweep:
+# gen="host": traces from numpy (the reference's own draws); gen="device": the same traces
+# generated on the GPU by slosim_gen_longtail (bit-identical, tests/test_gpu_longtail.py).
+def _traces(specs, gen: str) -> list:
+    if gen == "device":
+        return longtail_arrays_device(specs)
+    if gen != "host":
+        raise ValueError(f"gen must be 'host' or 'device', not {gen!r}")
+    return [longtail_arrays(s) for s in specs]
+
+
+def config1(gen: str = "host", **kw) -> Sweep:
     """gen_longtail(LongTailSpec()) x 6 CLI rates x 2 pairs (12 instances)."""
-    base = longtail_arrays(LongTailSpec())
+    base, = _traces([LongTailSpec()], gen)
     return grid_batch([base], CONFIG1_RATES, [1.0], PAIRS_2, name="config1", **kw)
 
 
-def config2(**kw) -> Sweep:
+def config2(gen: str = "host", **kw) -> Sweep:
     """One 100k-request trace at qps 1.0, kairos and fcfs pairs (2 instances)."""
-    base = longtail_arrays(LongTailSpec(n_requests=100_000, seed=2024, qps=1.0))
+    base, = _traces([LongTailSpec(n_requests=100_000, seed=2024, qps=1.0)], gen)
     return grid_batch([base], None, [1.0], PAIRS_2[::-1], name="config2", **kw)
 
 
-def config3(**kw) -> Sweep:
+def config3(gen: str = "host", **kw) -> Sweep:
     """Config-1 trace x 64 rates x 16 SLO scales x 3 pairs (3072 instances)."""
-    base = longtail_arrays(LongTailSpec())
+    base, = _traces([LongTailSpec()], gen)
     return grid_batch([base], SWEEP_RATES, SWEEP_SLO_SCALES, PAIRS_3, name="config3", **kw)
 
 
@@ -157,17 +167,17 @@ def split_round_robin(tr: TraceArrays, k: int) -> list:
     return out
 
 
-def config4(seeds=range(256), n_requests=20_000, **kw) -> Sweep:
+def config4(seeds=range(256), n_requests=20_000, gen: str = "host", **kw) -> Sweep:
     """256 seeds x 20k requests at qps 4.0, split into 4 1P+1D pairs each, x 2 pairs (2048 instances)."""
     traces = []
-    for s in seeds:
-        traces += split_round_robin(longtail_arrays(LongTailSpec(n_requests=n_requests, seed=int(s), qps=4.0)), 4)
+    for tr in _traces([LongTailSpec(n_requests=n_requests, seed=int(s), qps=4.0) for s in seeds], gen):
+        traces += split_round_robin(tr, 4)
     return grid_batch(traces, None, [1.0], PAIRS_2, name="config4", **kw)
 
 
-def config5(seeds=range(256), select=None, **kw) -> Sweep:
+def config5(seeds=range(256), select=None, gen: str = "host", **kw) -> Sweep:
     """256 seeds x 64 rates x 16 SLO scales x 4 pairs = 1,048,576 instances of 1k requests."""
-    traces = [longtail_arrays(LongTailSpec(seed=int(s))) for s in seeds]
+    traces = _traces([LongTailSpec(seed=int(s)) for s in seeds], gen)
     return grid_batch(traces, SWEEP_RATES, SWEEP_SLO_SCALES, PAIRS_4, name="config5", select=select, **kw)
 
 

@@ -936,6 +936,12 @@ extern "C" const char* slosim_build_info(void) {
 
 extern "C" const char* slosim_last_error(void) { return g_err; }
 
+// For the other translation units (longtail.cu): record a CUDA error for slosim_last_error.
+int slosim_internal_fail(int code, const char* what, cudaError_t e) {
+    fail_cuda(e, what);
+    return code;
+}
+
 // ---------------------------------------------------------------- exchange --
 namespace {
 // NCCL entry points resolved at run time (no link-time dependency; an already

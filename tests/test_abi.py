@@ -65,6 +65,8 @@ int main(void) {
   P(slosim_summary_t, tps_p50) P(slosim_summary_t, digest) P(slosim_summary_t, max_active)
   P(slosim_batch_t, profiles) P(slosim_batch_t, instances) P(slosim_batch_t, rows) P(slosim_batch_t, max_requests)
   P(slosim_batch_t, order) P(slosim_batch_t, rows_capacity) P(slosim_batch_t, trace_buf_capacity)
+  P(slosim_longtail_spec_t, p_long) P(slosim_longtail_spec_t, seed) P(slosim_longtail_spec_t, offset)
+  printf("sizeof.longtail %zu\n", sizeof(slosim_longtail_spec_t));
   return 0;
 }
 """
@@ -77,11 +79,11 @@ def test_struct_layouts_match_ctypes(tmp_path):
     subprocess.run(["gcc", "-I", os.path.join(ROOT, "include"), "-o", str(exe), str(src)], check=True)
     vals = dict(line.split() for line in subprocess.run([str(exe)], capture_output=True, text=True).stdout.splitlines())
     m = {"profile": _abi.Profile, "instance": _abi.Instance, "summary": _abi.Summary, "batch": _abi.Batch,
-         "rows": _abi.Rows}
+         "rows": _abi.Rows, "longtail": _abi.LongTailSpec}
     for k, cls in m.items():
         assert int(vals[f"sizeof.{k}"]) == ctypes.sizeof(cls), k
     names = {"slosim_profile_t": _abi.Profile, "slosim_instance_t": _abi.Instance, "slosim_summary_t": _abi.Summary,
-             "slosim_batch_t": _abi.Batch}
+             "slosim_batch_t": _abi.Batch, "slosim_longtail_spec_t": _abi.LongTailSpec}
     for key, v in vals.items():
         if key.startswith("sizeof"):
             continue
