@@ -130,6 +130,29 @@ __device__ __forceinline__ double llookup(const Arr<double, WL>& M, const LGeo& 
     return xadd(v1, xmul(xmul(xsub(v2, v1), (double)(bsz - (1 << lo))), pow2_neg(lo)));
 }
 
+// llookup with a one-entry memo: within one Alg. 3 scan the LUT is fixed, and consecutive candidates
+// often share the (|B|+1, column) key (sequences below the first bucket edge all select column 0).
+struct LMemo { int bsz, c; double dx, v; };
+__device__ __forceinline__ double llookup_memo(const Arr<double, WL>& M, const LGeo& g, int bsz, int seq, LMemo& mm) {
+    const int w = 1 << g.wsh;
+    int c = (seq >> g.wsh) - 1;
+    const bool in = seq > w && c < g.ns - 1;
+    c = in ? c : (seq <= w ? 0 : g.ns - 1);
+    const double dx = in ? (double)(seq & (w - 1)) : 0.0;
+    if (bsz == mm.bsz && c == mm.c && dx == mm.dx) return mm.v;
+    const int i = gbidx(bsz);
+    const bool single = (i == 0) | (i >= g.nb) | ((1u << i) == (unsigned)bsz);
+    const int lo = i >= g.nb ? g.nb - 1 : (i == 0 ? 0 : i - 1);
+    const int r1 = single ? (i >= g.nb ? g.nb - 1 : i) : lo;
+    double v = lrow(M, g, r1, c, dx);
+    if (!single) {
+        const double v2 = lrow(M, g, i, c, dx);
+        v = xadd(v, xmul(xmul(xsub(v2, v), (double)(bsz - (1 << lo))), pow2_neg(lo)));
+    }
+    mm = LMemo{bsz, c, dx, v};
+    return v;
+}
+
 // RN(a/x) > RN(b/y) (decode_sched.py:87-89), see numerics.cuh quot_gt.
 __device__ __noinline__ bool lquot_exact(double a, double x, double b, double y) { return __ddiv_rn(a, x) > __ddiv_rn(b, y); }
 __device__ __forceinline__ bool lquot_gt(double a, double x, double b, double y) {
@@ -439,11 +462,32 @@ __device__ __forceinline__ void ladmit(St& S, const LCtx& cx, const LWs& w) {
         // kairos: keep the active set in (seq_len, id) order (decode_sched.py:74)
         int k = S.an;
         if (S.dpol == SLOSIM_DECODE_KAIROS_SLACK) {
+#ifndef SLOSIM_LANE_NO_PREFETCH_ADMIT
+            // shift the entries that sort after the new one up by one; entry k-2 is loaded while
+            // entry k-1 is stored at k
+            if (k > 0) {
+                int32_t s_ = AS[k - 1], i_ = AI[k - 1], p_ = AP[k - 1], o_ = AO[k - 1], n_ = AN[k - 1],
+                        m_ = AM[k - 1], f_ = AF[k - 1];
+                int64_t t_ = AT[k - 1];
+                while (k > 0 && (s_ > inp || (s_ == inp && i_ > idr))) {
+                    int32_t s2 = 0, i2 = 0, p2 = 0, o2 = 0, n2 = 0, m2 = 0, f2 = 0;
+                    int64_t t2 = 0;
+                    if (k > 1) {
+                        s2 = AS[k - 2]; i2 = AI[k - 2]; p2 = AP[k - 2]; o2 = AO[k - 2]; n2 = AN[k - 2];
+                        m2 = AM[k - 2]; f2 = AF[k - 2]; t2 = AT[k - 2];
+                    }
+                    AP[k] = p_; AS[k] = s_; AI[k] = i_; AO[k] = o_; AN[k] = n_; AM[k] = m_; AF[k] = f_; AT[k] = t_;
+                    s_ = s2; i_ = i2; p_ = p2; o_ = o2; n_ = n2; m_ = m2; f_ = f2; t_ = t2;
+                    k--;
+                }
+            }
+#else
             while (k > 0 && (AS[k - 1] > inp || (AS[k - 1] == inp && AI[k - 1] > idr))) {
                 AP[k] = AP[k - 1]; AS[k] = AS[k - 1]; AI[k] = AI[k - 1]; AO[k] = AO[k - 1]; AN[k] = AN[k - 1];
                 AM[k] = AM[k - 1]; AF[k] = AF[k - 1]; AT[k] = AT[k - 1];
                 k--;
             }
+#endif
         }
         AP[k] = pos; AS[k] = inp; AI[k] = idr; AO[k] = outl; AN[k] = inp; AM[k] = 0; AF[k] = ttm ? 2 : 0; AT[k] = ttr;
         S.an++;
@@ -577,6 +621,55 @@ __device__ __forceinline__ void ldecode_done(St& S, const LWs& w, int64_t t) {
     const bool kairos = S.dpol == SLOSIM_DECODE_KAIROS_SLACK;
     bool moved = false;  // a member now sorts before an earlier entry (kairos order repair below)
     int32_t pseq = -1, pidr = -1;
+#ifndef SLOSIM_LANE_NO_PREFETCH
+    // software-pipelined: entry k+1 is loaded while entry k is processed (stores go to o <= k)
+    int32_t n_seq = 0, n_fl = 0, n_idr = 0, n_pos = 0, n_inp = 0, n_out = 0, n_miss = 0;
+    int64_t n_tf = 0;
+    if (an > 0) {
+        n_seq = AS[0]; n_fl = AF[0]; n_idr = AI[0]; n_pos = AP[0]; n_inp = AN[0]; n_out = AO[0]; n_miss = AM[0];
+        n_tf = AT[0];
+    }
+    for (int k = 0; k < an; k++) {
+        int32_t seq = n_seq;
+        const int32_t fl = n_fl, idr = n_idr, pos = n_pos, inp = n_inp, outl = n_out, miss0 = n_miss;
+        const int64_t tf = n_tf;
+        if (k + 1 < an) {
+            n_seq = AS[k + 1]; n_fl = AF[k + 1]; n_idr = AI[k + 1]; n_pos = AP[k + 1]; n_inp = AN[k + 1];
+            n_out = AO[k + 1]; n_miss = AM[k + 1]; n_tf = AT[k + 1];
+        }
+        if (pre >= 0 ? k < pre : (fl & 1)) {
+            seq += 1;
+            const int ngen = seq - inp;
+            hs += member_hash((uint32_t)pos);
+            const int32_t miss = miss0 + (t > tf + (int64_t)ngen * S.tpot_slo ? 1 : 0);
+            if (ngen == outl - 1) {  // retires: request_metrics (metrics.py:72-84)
+                const int64_t span = t - tf;
+                const double tpot = idiv(span, (int64_t)(outl - 1));
+                const bool tpm = tpot <= (double)S.tpot_slo;
+                TP[S.ntps] = xdiv((double)(outl - 1), xdiv((double)span, 1e6));
+                S.ntps++;
+                S.misses += miss;
+                S.c_tpot += tpm;
+                S.c_e2e += tpm && (fl & 2);
+                S.finished++;
+                kv_rel += (int64_t)inp + outl;
+                continue;
+            }
+            if (o != k) { AP[o] = pos; AN[o] = inp; AO[o] = outl; AT[o] = tf; AI[o] = idr; }
+            AM[o] = miss;
+            AS[o] = seq;
+            AF[o] = fl & ~1;
+        } else if (o != k) {
+            AP[o] = pos; AN[o] = inp; AO[o] = outl; AT[o] = tf; AI[o] = idr; AM[o] = miss0; AS[o] = seq;
+            AF[o] = fl;
+        }
+        if (kairos) moved |= seq < pseq || (seq == pseq && idr < pidr);
+        pseq = seq;
+        pidr = idr;
+        mx = seq > mx ? seq : mx;
+        o++;
+    }
+#else
     for (int k = 0; k < an; k++) {
         int32_t seq = AS[k];
         const int32_t fl = AF[k];
@@ -615,6 +708,7 @@ __device__ __forceinline__ void ldecode_done(St& S, const LWs& w, int64_t t) {
         mx = seq > mx ? seq : mx;
         o++;
     }
+#endif
     S.an = o;
     S.amax = mx;
     S.kv -= kv_rel;
@@ -678,9 +772,27 @@ __device__ __forceinline__ void ldecode_start(St& S, const LWs& w, int64_t t) {
             }
             const double smin = xsub((double)vmin, llookup(M, g, an, bmax));
             double tcur = 0.0;
+            LMemo mm{-1, -1, 0.0, 0.0};
+#ifndef SLOSIM_LANE_NO_SCAN_FLAGS
+            // candidate k+1's key and flag word are loaded while candidate k is decided
+            int nseq = AS[0], nfl = AF[0];
             for (int k = 0; k < an; k++) {
-                const int seq = AS[k];
-                const double ts = llookup(M, g, b + 1, seq);
+                const int seq = nseq, fl = nfl;
+                if (k + 1 < an) { nseq = AS[k + 1]; nfl = AF[k + 1]; }
+                const double ts = llookup_memo(M, g, b + 1, seq, mm);
+                if (ts <= smin && (b == 0 || lquot_gt((double)(b + 1), ts, (double)b, tcur))) {
+                    AF[k] = fl | 1;
+                    b++;
+                    tcur = ts;
+                    ms = seq;
+                }
+            }
+#else
+            int nseq = AS[0];
+            for (int k = 0; k < an; k++) {
+                const int seq = nseq;
+                if (k + 1 < an) nseq = AS[k + 1];
+                const double ts = llookup_memo(M, g, b + 1, seq, mm);
                 if (ts <= smin && (b == 0 || lquot_gt((double)(b + 1), ts, (double)b, tcur))) {
                     AF[k] |= 1;
                     b++;
@@ -688,12 +800,22 @@ __device__ __forceinline__ void ldecode_start(St& S, const LWs& w, int64_t t) {
                     ms = seq;
                 }
             }
+#endif
         }
         if (b > 0) {
             bsz = b;
             bmax = ms;
         } else {
+#ifndef SLOSIM_LANE_NO_SCAN_FLAGS
+            int fl = AF[0];  // fallback: the whole active set
+            for (int k = 0; k < an; k++) {
+                const int f = fl;
+                if (k + 1 < an) fl = AF[k + 1];
+                AF[k] = f | 1;
+            }
+#else
             for (int k = 0; k < an; k++) AF[k] |= 1;  // fallback: the whole active set
+#endif
         }
     } else {
         S.dc_prefix = an;

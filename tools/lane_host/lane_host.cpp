@@ -56,7 +56,7 @@ extern "C" int lane_host_run_batch(const slosim_batch_t* B) {
     for (int p = 0; p < B->n_profiles; p++) host_table(&tabs[p], B->profiles + p);
     int64_t cap = 1;
     for (int64_t i = 0; i < B->n_instances; i++) cap = std::max<int64_t>(cap, B->instances[i].n_requests);
-    LCtx cx;
+    LCtx cx{};
     cx.B = *B;
     cx.B.max_requests = cap;
     cx.sched_tab = tabs.data();
