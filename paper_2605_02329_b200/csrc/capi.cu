@@ -184,9 +184,12 @@ extern "C" int slosim_run_batch(const slosim_batch_t* b, void* stream) {
     const int64_t lane_slots = (int64_t)ds.sms * ds.lane_blocks_per_sm * 128;
     const bool lane_path = !full && !force_lat && !getenv("SLOSIM_NO_LANE_ENGINE") &&
                            (b->n_instances >= lane_slots || getenv("SLOSIM_FORCE_LANE_ENGINE"));
-    const bool solo = getenv("SLOSIM_LANE_SOLO") != nullptr && !full && !force_lat;  // experiment knob
-    if (lane_path || solo) {
-        const int64_t per_block = solo ? 4 : 128;
+    // experiment knob: lane engine with k live lanes per warp (k = 1: one instance per warp)
+    int lpw = 32;
+    if (const char* e = getenv("SLOSIM_LANE_LPW")) lpw = std::max(1, std::min(32, atoi(e)));
+    const bool narrow = lpw < 32 && !full && !force_lat;
+    if (lane_path || narrow) {
+        const int64_t per_block = 4 * (int64_t)lpw;
         int64_t lblocks = std::min<int64_t>((b->n_instances + per_block - 1) / per_block,
                                             (int64_t)ds.sms * ds.lane_blocks_per_sm);
         size_t lstride = lane::lws_bytes(cap, LUT_CELLS);
@@ -199,7 +202,7 @@ extern "C" int slosim_run_batch(const slosim_batch_t* b, void* stream) {
         lc.sched_tab = sched;
         lc.deferred = (int64_t*)ds.defer.ptr;
         lc.n_deferred = ctr + 1;
-        lane::lane_kernel<<<(int)lblocks, 128, 0, st>>>(lc, (char*)ds.lws.ptr, cap, LUT_CELLS, ctr, solo ? 1 : 0);
+        lane::lane_kernel<<<(int)lblocks, 128, 0, st>>>(lc, (char*)ds.lws.ptr, cap, LUT_CELLS, ctr, lpw);
         CK(cudaGetLastError());
         cx.B.order = (const int64_t*)ds.defer.ptr;
         cx.dyn_n = ctr + 1;

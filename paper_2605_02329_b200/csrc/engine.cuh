@@ -1072,6 +1072,78 @@ __device__ __noinline__ int64_t on_retire(Sim& S, const Slot sl, int64_t t, bool
     return wsum64(kv_rel);
 }
 
+// DecodeStepLUT.lookup (costmodel.py:157-187) on the full power-of-two grid from the cell means,
+// with cell c0's mean replaced by m0 (ff_verify): the np.interp slope of a column pair is formed
+// from the means exactly as lut_build/gupdate store it, RN((m[c+1] - m[c]) * 2^-wsh), and the
+// rows combine as in geval_p.
+__device__ __forceinline__ double ff_row(const double* M, const Geo& g, double inv_w, int r, const ColSel& cs, int c0,
+                                         double m0) {
+    const int k = r * g.ns + cs.c;
+    const double a = k == c0 ? m0 : M[k];
+    if (cs.dx == 0.0) return a;
+    const double b = k + 1 == c0 ? m0 : M[k + 1];
+    return xadd(xmul(xmul(xsub(b, a), inv_w), cs.dx), a);
+}
+__device__ __forceinline__ double ff_lookup(const LutMem* L, const Geo& g, double inv_w, const RowP& rp, int seq,
+                                            int c0, double m0) {
+    const ColSel cs = gcol(g, seq);
+    const double v1 = ff_row(L->mean, g, inv_w, rp.r1, cs, c0, m0);
+    const double v2 = rp.r2 == rp.r1 ? v1 : ff_row(L->mean, g, inv_w, rp.r2, cs, c0, m0);
+    return xadd(v1, xmul(xmul(xsub(v2, v1), (double)rp.num), rp.inv));
+}
+__device__ __forceinline__ bool ff_quot_gt(double a, double x, double b, double y) {
+    bool tie;
+    const bool gt = quot_gt_fast(a, x, b, y, tie);
+    return tie ? quot_gt_exact(a, x, b, y) : gt;
+}
+
+// ff_steps<.., V = true>: lane k verifies that the step started at e_k (after completions 0..k of
+// the run, each of them batching the whole active set A) batches A again.  `e` is this lane's e_k;
+// `rank` the lane's (seq_len, id) rank among A at time t (scan_geo's cache).
+__device__ __noinline__ bool ff_verify(const Sim& S, const Slot& sl, int64_t t, int64_t e, int lane, const RowP* rowtab,
+                                       int rank) {
+    const bool occ = (S.amask >> lane) & 1u;
+    const int an = S.an;
+    const int64_t tpot = S.tpot_slo;
+    // the active set's sequence lengths in rank order (per-warp shared memory)
+    __shared__ int32_t ff_seq[4][32];
+    int32_t* rs = ff_seq[threadIdx.x >> 5];
+    __syncwarp();
+    if (occ) rs[rank] = sl.seq;
+    // slack (decode_sched.py:36-57) at step k+1: tpot*(n_gen + k + 2) - (e_k - t_first)
+    const int64_t v0 = wmin64_redux(occ ? tpot * ((int64_t)(sl.seq - sl.inp) + 1) + sl.tf : SLOSIM_INF64);
+    __syncwarp();
+    const LutMem* L = S.L;
+    const Geo g = geo_of(L);
+    const double inv_w = pow2_neg(g.wsh);
+    const int kk = lane + 1;  // completions applied before step k+1 starts
+    // cell c0 after kk completions: exact integer sum (checked integral by the caller's commit) over count
+    const int i0 = min(gbidx(an), g.nb - 1);
+    const int j0 = min((int)((S.dc_max + (1 << g.wsh) - 1) >> g.wsh) - 1, g.ns - 1);
+    const int c0 = i0 * g.ns + j0;
+    const double s0 = L->sum[c0];
+    if (!(s0 == rint(s0) && fabs(s0) + (double)(e - t) < 0x1p53)) return false;
+    const double m0 = xdiv(xadd(s0, (double)(e - t)), (double)(L->cnt[c0] + kk));
+    const int64_t vmin = v0 + (int64_t)kk * tpot - e;
+    const double fb = ff_lookup(L, g, inv_w, rowtab[an], (int)S.amax + kk, c0, m0);
+    const double smin = xsub((double)vmin, fb);
+    // greedy scan admitting every candidate in (seq_len, id) order
+    bool all = true;
+    double xp = 0.0;
+#pragma unroll 1
+    for (int r = 0; r < an; r++) {
+        const double x = ff_lookup(L, g, inv_w, rowtab[r + 1], rs[r] + kk, c0, m0);
+        if (!(x <= smin && (r == 0 || ff_quot_gt((double)(r + 1), x, (double)r, xp)))) { all = false; break; }
+        xp = x;
+    }
+    if (all) return true;
+    // or admitting none (every candidate rejected against the empty batch): the fallback batches A
+#pragma unroll 1
+    for (int r = 0; r < an; r++)
+        if (ff_lookup(L, g, inv_w, rowtab[1], rs[r] + kk, c0, m0) <= smin) return false;
+    return true;
+}
+
 // Decode steps between rare events, applied in bulk.  Under continuous
 // batching (decode_sched.py:114-124) the batch is the whole active set; under
 // Alg. 3 with a single active request it is that request whatever the scan
@@ -1090,10 +1162,24 @@ __device__ __noinline__ int64_t on_retire(Sim& S, const Slot sl, int64_t t, bool
 // m, and the mean and slopes are recomputed once from the final sums.  Step m
 // is left in progress exactly as the loop would have started it.  Returns m.
 // Preconditions (checked by the caller): register mode, plain formula ground
-// truth, no per-step trace, no pending prefill start; LUTUPD: one active
-// request and a fully populated LUT.
-template <bool LUTUPD, bool G>
-__device__ __noinline__ int ff_steps(Sim& S, Slot& sl, int64_t t, int lane) {
+// truth, no per-step trace, no pending prefill start; LUTUPD: a fully
+// populated LUT and either one active request or (V) a batch that is the whole
+// active set.
+//
+// V (Alg. 3 with |A| > 1, the step just started batching all of A): the
+// decision of every later step in the run is verified instead of assumed.
+// Lane k re-runs select_decode_batch (decode_sched.py:60-111) for step k+1 as
+// the loop would see it at time e_k: every request advanced by k+1 tokens (so
+// the (seq_len, id) order is unchanged), the slack minimum shifted by
+// (k+1)*tpot - (e_k - t), and the LUT as the k+1 earlier completions leave it
+// (only cell c0 differs: its exact integer sum over its count; lookups read
+// means and form the np.interp slopes as the stored slopes are formed).  The
+// step batches A again iff the greedy scan admits every candidate, or none
+// (the fallback).  The run is the leading prefix of steps whose completion is
+// pure and whose successor's decision is verified.
+template <bool LUTUPD, bool G, bool V = false>
+__device__ __noinline__ int ff_steps(Sim& S, Slot& sl, int64_t t, int lane, const RowP* rowtab = nullptr,
+                                     int rank = 0) {
     const bool occ = (S.amask >> lane) & 1u;
     const int64_t ng = (int64_t)sl.seq - sl.inp;  // tokens generated before step 0
     const int r = __reduce_min_sync(FULLMASK, occ ? (int)(sl.out - 2 - ng) : 0x7fffffff);
@@ -1116,9 +1202,15 @@ __device__ __noinline__ int ff_steps(Sim& S, Slot& sl, int64_t t, int lane) {
         const int j0 = __shfl_sync(FULLMASK, j, 0);  // unconditional: every lane takes part
         pure = pure && j == j0;
     }
+    if (V) {  // every lane takes part in the verification's collectives
+        const bool vf = ff_verify(S, sl, t, e, lane, rowtab, rank);
+        pure = pure && vf;
+    }
     // end times increase and the other bounds are thresholds, so the pure steps form a prefix
-    const int m = __popc(__ballot_sync(FULLMASK, pure));
-    if (m == 0) return 0;
+    // (V: the leading run of verified steps)
+    const unsigned pm = __ballot_sync(FULLMASK, pure);
+    const int m = V ? __ffs((int)~pm) - 1 : __popc(pm);
+    if (m <= 0) return 0;
     if (LUTUPD) {
         const int64_t dsum = wsum64(lane < m ? d : 0);
         const int nb = L->nb, ns = L->ns;
@@ -1153,6 +1245,16 @@ __device__ __noinline__ int ff_steps(Sim& S, Slot& sl, int64_t t, int lane) {
     S.amax += m;
     return m;
 }
+
+// Verified multi-step fast-forward of Alg. 3 runs: a latency-build feature.  In the throughput
+// build the other resident warps use the issue slots a failed verification costs (configs 3 and 4:
+// 213 -> 265 ms and 685 -> 1045 ms with it), in the latency build nothing else would (config 2:
+// 6.78 -> 5.73 s, config 1: 83 -> 66 ms).
+#if defined(SLOSIM_NO_FF_MULTI) || !defined(SLOSIM_MIN_BLOCKS) || SLOSIM_MIN_BLOCKS != 1
+#define FF_MULTI false
+#else
+#define FF_MULTI true
+#endif
 
 #ifdef SLOSIM_NO_FF_KAIROS
 #define FF_KAIROS false
@@ -1472,14 +1574,18 @@ __device__ SIM_INLINE void simulate(const Ctx& cx, int64_t ii, const WS& w, int 
             dc_max = bmax;
             dc_end = t + dc_dur;
 #ifndef SLOSIM_NO_FF
-            if ((DP == SLOSIM_DECODE_CONTINUOUS ? !use_lut : (FF_KAIROS && an == 1)) &&
+            // Alg. 3 runs that batch the whole active set again and again (|A| > 1) are verified
+            // step by step (ff_steps<.., V>); the geometry scan keeps the ranks they need
+            const bool ff_multi = DP == SLOSIM_DECODE_KAIROS_SLACK && FF_MULTI && G && an > 1 && bsz == an;
+            if ((DP == SLOSIM_DECODE_CONTINUOUS ? !use_lut : (FF_KAIROS && (an == 1 || ff_multi))) &&
                 (DP == SLOSIM_DECODE_CONTINUOUS || lut_full) && regmode && gt_plain && !(FULL && S.T.buf) &&
                 dc_end < t_rare && !pf_wait) {
                 PROF_MARK(3);
                 SIM_SYNC_OUT();
                 S.sl = sl;
                 const int m = DP == SLOSIM_DECODE_CONTINUOUS ? ff_steps<false, false>(S, S.sl, t, lane)
-                                                             : ff_steps<true, G>(S, S.sl, t, lane);
+                              : an == 1                      ? ff_steps<true, G>(S, S.sl, t, lane)
+                                                             : ff_steps<true, G, FF_MULTI>(S, S.sl, t, lane, rowtab, rk_rank);
                 sl = S.sl;
                 SIM_SYNC_IN();
                 PROF_MARK(4);

@@ -873,7 +873,7 @@ __device__ __forceinline__ bool lstep(St& S, const LCtx& cx, const LWs& w) {
 // Persistent lane engine: each lane pulls instances (in `order`) from the work counter.
 __global__ void __launch_bounds__(128, SLOSIM_LANE_MIN_BLOCKS)
     lane_kernel(const __grid_constant__ LCtx cx, char* ws_base, int64_t cap, int cells, unsigned long long* work,
-                int solo) {
+                int lanes_per_warp) {
     const int lane = threadIdx.x & 31;
     const int64_t gw = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     const size_t warp_bytes = lws_bytes(cap, cells);
@@ -881,9 +881,9 @@ __global__ void __launch_bounds__(128, SLOSIM_LANE_MIN_BLOCKS)
     const int64_t N = cx.B.n_instances;
     St S;
     S.ii = 0;
-    // live: an instance in progress; done: the work queue is drained.  Solo launches (small batches,
-    // where per-instance latency decides) run one instance per warp, on lane 0.
-    bool live = false, done = solo && lane != 0;
+    // live: an instance in progress; done: the work queue is drained.  Launches of small batches,
+    // where per-instance latency decides, use only lanes [0, lanes_per_warp) of each warp.
+    bool live = false, done = lane >= lanes_per_warp;
     for (;;) {
         if (!live && !done) {
             // pull the next instance (one atomic per warp for all lanes that need work)

@@ -30,7 +30,7 @@ np.save(OUTF, np.concatenate(out))
 '''
 res = {}
 for name, env in [("warp_lat", {"SLOSIM_FORCE_LATENCY_ENGINE": "1"}), ("lane", {"SLOSIM_FORCE_LANE_ENGINE": "1"}),
-                  ("lane_solo", {"SLOSIM_LANE_SOLO": "1"})]:
+                  ("lane_solo", {"SLOSIM_LANE_LPW": "1"})]:
     outf = f"/tmp/c2_{name}.npy"
     code = (CHILD.replace("ROOT", repr(ROOT)).replace("NREQ", str(n_req)).replace("OUTF", repr(outf))
             .replace("ENGINE", repr(name)))
