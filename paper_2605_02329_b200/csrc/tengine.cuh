@@ -40,6 +40,10 @@
 #include "lut.cuh"
 #include "warpops.cuh"
 
+#if defined(SLOSIM_LANE_NO_PREFETCH) && !defined(SLOSIM_LANE_NO_VBASE)
+#define SLOSIM_LANE_NO_VBASE  // the slack base is kept by the software-pipelined member loop only
+#endif
+
 namespace slosim {
 namespace lane {
 
@@ -217,6 +221,12 @@ struct St {
     int32_t c_ttft, c_tpot, c_e2e, ntps, max_q, max_a, finished;
     int64_t misses, worst_wait, psteps, dsteps, v_dec, b_dec, v_pre, t_end;
     uint64_t D;
+#ifndef SLOSIM_LANE_NO_VBASE
+    // Alg. 3 slack base: min over the active set of tpot*(n_gen+1) + t_first, so that the slack
+    // minimum at time t (decode_sched.py:36-57, 89-90) is vbase - t - fallback; kept by the
+    // member loop, admission and retirement instead of a pass over the active set per step
+    int64_t vbase;
+#endif
 };
 
 // Rarely used per-instance parameters are read from the descriptor (not kept in registers).
@@ -299,6 +309,9 @@ __device__ __forceinline__ bool linit(St& S, const LCtx& cx, const LWs& w, int64
     S.c_ttft = S.c_tpot = S.c_e2e = S.ntps = S.max_q = S.max_a = S.finished = 0;
     S.misses = S.worst_wait = S.psteps = S.dsteps = S.v_dec = S.b_dec = S.v_pre = S.t_end = 0;
     S.D = 0;
+#ifndef SLOSIM_LANE_NO_VBASE
+    S.vbase = SLOSIM_INF64;
+#endif
     return true;
 }
 
@@ -490,6 +503,9 @@ __device__ __forceinline__ void ladmit(St& S, const LCtx& cx, const LWs& w) {
 #endif
         }
         AP[k] = pos; AS[k] = inp; AI[k] = idr; AO[k] = outl; AN[k] = inp; AM[k] = 0; AF[k] = ttm ? 2 : 0; AT[k] = ttr;
+#ifndef SLOSIM_LANE_NO_VBASE
+        S.vbase = min(S.vbase, ttr + S.tpot_slo);
+#endif
         S.an++;
         S.amax = inp > S.amax ? inp : S.amax;
     }
@@ -629,6 +645,9 @@ __device__ __forceinline__ void ldecode_done(St& S, const LWs& w, int64_t t) {
         n_seq = AS[0]; n_fl = AF[0]; n_idr = AI[0]; n_pos = AP[0]; n_inp = AN[0]; n_out = AO[0]; n_miss = AM[0];
         n_tf = AT[0];
     }
+#ifndef SLOSIM_LANE_NO_VBASE
+    int64_t vb = SLOSIM_INF64;
+#endif
     for (int k = 0; k < an; k++) {
         int32_t seq = n_seq;
         const int32_t fl = n_fl, idr = n_idr, pos = n_pos, inp = n_inp, outl = n_out, miss0 = n_miss;
@@ -641,7 +660,11 @@ __device__ __forceinline__ void ldecode_done(St& S, const LWs& w, int64_t t) {
             seq += 1;
             const int ngen = seq - inp;
             hs += member_hash((uint32_t)pos);
-            const int32_t miss = miss0 + (t > tf + (int64_t)ngen * S.tpot_slo ? 1 : 0);
+            const int64_t dl = tf + (int64_t)ngen * S.tpot_slo;  // this token's deadline (metrics.py:57-69)
+            const int32_t miss = miss0 + (t > dl ? 1 : 0);
+#ifndef SLOSIM_LANE_NO_VBASE
+            if (ngen != outl - 1) vb = min(vb, dl + S.tpot_slo);
+#endif
             if (ngen == outl - 1) {  // retires: request_metrics (metrics.py:72-84)
                 const int64_t span = t - tf;
                 const double tpot = idiv(span, (int64_t)(outl - 1));
@@ -659,9 +682,14 @@ __device__ __forceinline__ void ldecode_done(St& S, const LWs& w, int64_t t) {
             AM[o] = miss;
             AS[o] = seq;
             AF[o] = fl & ~1;
-        } else if (o != k) {
-            AP[o] = pos; AN[o] = inp; AO[o] = outl; AT[o] = tf; AI[o] = idr; AM[o] = miss0; AS[o] = seq;
-            AF[o] = fl;
+        } else {
+#ifndef SLOSIM_LANE_NO_VBASE
+            if (kairos) vb = min(vb, tf + ((int64_t)(seq - inp) + 1) * S.tpot_slo);
+#endif
+            if (o != k) {
+                AP[o] = pos; AN[o] = inp; AO[o] = outl; AT[o] = tf; AI[o] = idr; AM[o] = miss0; AS[o] = seq;
+                AF[o] = fl;
+            }
         }
         if (kairos) moved |= seq < pseq || (seq == pseq && idr < pidr);
         pseq = seq;
@@ -712,6 +740,9 @@ __device__ __forceinline__ void ldecode_done(St& S, const LWs& w, int64_t t) {
     S.an = o;
     S.amax = mx;
     S.kv -= kv_rel;
+#ifndef SLOSIM_LANE_NO_VBASE
+    S.vbase = vb;
+#endif
     if (moved) {
         // members moved up by one token: restore (seq_len, id) order by insertion
         for (int k = 1; k < o; k++) {
@@ -765,11 +796,15 @@ __device__ __forceinline__ void ldecode_start(St& S, const LWs& w, int64_t t) {
         if (an > 1) {
             const auto M = w.mean();
             const LGeo& g = S.g;
+#ifndef SLOSIM_LANE_NO_VBASE
+            const int64_t vmin = S.vbase - t;
+#else
             int64_t vmin = SLOSIM_INF64;
             for (int k = 0; k < an; k++) {
                 const int64_t v = S.tpot_slo * ((int64_t)(AS[k] - AN[k]) + 1) - (t - AT[k]);
                 vmin = v < vmin ? v : vmin;
             }
+#endif
             const double smin = xsub((double)vmin, llookup(M, g, an, bmax));
             double tcur = 0.0;
             LMemo mm{-1, -1, 0.0, 0.0};

@@ -119,3 +119,22 @@ def test_random_instances_equal_oracle_lane_engine(monkeypatch):
         a, b = got[k], want[k]
         eq = np.array_equal(a, b, equal_nan=True) if a.dtype.kind == "f" else np.array_equal(a, b)
         assert eq, (k, int(np.flatnonzero(a != b)[0]) if not eq and a.dtype.kind != "f" else None)
+
+
+def test_random_instances_equal_oracle_latency_build(monkeypatch):
+    """The same random sweep forced through the latency build (one 4-warp block per SM), whose Alg. 3
+    runs are fast-forwarded with per-step verification (ff_steps<.., V>): every power-of-two-grid
+    kairos-slack instance with more than one request active takes that path whenever a step batches
+    the whole active set."""
+    from oracle import oracle
+    from paper_2605_02329_b200.batch import run_batch
+
+    monkeypatch.setenv("SLOSIM_FORCE_LATENCY_ENGINE", "1")
+    got = run_batch(_batch()).copy()
+    ref = _batch(synth=oracle.synth)
+    oracle.run_batch(ref, threads=8)
+    want = ref.summaries
+    for k in [x for x in want.dtype.names if x != "sim_cycles"]:
+        a, b = got[k], want[k]
+        eq = np.array_equal(a, b, equal_nan=True) if a.dtype.kind == "f" else np.array_equal(a, b)
+        assert eq, (k, int(np.flatnonzero(a != b)[0]) if not eq and a.dtype.kind != "f" else None)
