@@ -60,17 +60,20 @@ struct Arr {
     __device__ __forceinline__ T& operator[](int k) const { return p[(size_t)k * STRIDE]; }
 };
 
-// Active set (interleaved), capacity `cap` requests.  A_FLAG bit 0: member of the running
-// Alg. 3 batch; bit 1: TTFT met.
-enum A32 { A_POS, A_SEQ, A_IDR, A_OUT, A_INP, A_MISS, A_FLAG, N_A32 };
+// Active set (interleaved), capacity `cap` requests: entry k of lane l is the 16-byte element
+// [k * 32 + l] of each of two vector arrays, V0 = {seq, flag, id_rank, pos} and
+// V1 = {input, output, misses, -}, plus t_first in an i64 array, so the member loop moves an
+// entry with three loads.  A_FLAG bit 0: member of the running Alg. 3 batch; bit 1: TTFT met.
+enum A32 { A_SEQ, A_FLAG, A_IDR, A_POS, A_INP, A_OUT, A_MISS, N_A32 };  // V0.x..w, V1.x..z
 enum A64 { A_TF, N_A64 };
+constexpr int A_VEC_BYTES = 2 * 16 + 8;  // per entry and lane
 
 __host__ __device__ inline size_t lws_lane_bytes(size_t c) {
     return N_WS_I32 * ws_align(4 * c) + N_WS_I64 * ws_align(8 * c);
 }
 __host__ __device__ inline size_t lws_bytes(int64_t cap, int cells) {
     size_t c = (size_t)(cap > 0 ? cap : 1);
-    return (size_t)WL * (c * (N_A32 * 4 + N_A64 * 8) + (size_t)cells * (8 + 8 + 4) + lws_lane_bytes(c));
+    return (size_t)WL * (c * A_VEC_BYTES + (size_t)cells * (8 + 8 + 4) + lws_lane_bytes(c));
 }
 
 // One warp's workspace: [active set, interleaved][LUT, interleaved][32 per-lane WS regions].
@@ -78,13 +81,16 @@ struct LWs {
     char* wb;  // warp base
     size_t c;
     int cells, lane;
-    __device__ __forceinline__ Arr<int32_t, WL> a32(int k) const {
-        return Arr<int32_t, WL>{(int32_t*)(wb + (size_t)k * WL * 4 * c) + lane};
+    __device__ __forceinline__ int4* v0() const { return (int4*)wb + lane; }
+    __device__ __forceinline__ int4* v1() const { return (int4*)(wb + (size_t)WL * 16 * c) + lane; }
+    // one field of the vector arrays (stride 4 ints per entry slot)
+    __device__ __forceinline__ Arr<int32_t, WL * 4> a32(int k) const {
+        return Arr<int32_t, WL * 4>{(int32_t*)(k < 4 ? v0() : v1()) + (k & 3)};
     }
     __device__ __forceinline__ Arr<int64_t, WL> a64(int k) const {
-        return Arr<int64_t, WL>{(int64_t*)(wb + (size_t)N_A32 * WL * 4 * c + (size_t)k * WL * 8 * c) + lane};
+        return Arr<int64_t, WL>{(int64_t*)(wb + (size_t)WL * 32 * c + (size_t)k * WL * 8 * c) + lane};
     }
-    __device__ __forceinline__ char* lut_base() const { return wb + (size_t)WL * c * (N_A32 * 4 + N_A64 * 8); }
+    __device__ __forceinline__ char* lut_base() const { return wb + (size_t)WL * c * A_VEC_BYTES; }
     __device__ __forceinline__ Arr<double, WL> mean() const { return Arr<double, WL>{(double*)lut_base() + lane}; }
     __device__ __forceinline__ Arr<double, WL> sum() const {
         return Arr<double, WL>{(double*)(lut_base() + (size_t)WL * 8 * cells) + lane};
@@ -105,14 +111,16 @@ struct LWs {
 // Python-form row interpolation on the power-of-two grid (lut.cuh lut_eval<true> / geval_p):
 // value of row r at column selection (c, dx) from the stored means; the np.interp slope of a
 // populated column pair is (m[c+1] - m[c]) * 2^-wsh, exactly as stored by lut_build / gupdate.
+// Scaling by a power of two is exact, so slope * dx = RN((m[c+1] - m[c]) * (dx * 2^-wsh)) with
+// dx * 2^-wsh exact: one rounding, one multiply (dxw below); likewise the weight across rows,
+// (bsz - 2^lo) * 2^-lo, is formed exactly and applied with one multiply.
 struct LGeo { int nb, ns, wsh; double inv_w; };
 
-__device__ __forceinline__ double lrow(const Arr<double, WL>& M, const LGeo& g, int r, int c, double dx) {
+__device__ __forceinline__ double lrow(const Arr<double, WL>& M, const LGeo& g, int r, int c, double dxw) {
     const int k = r * g.ns + c;
     const double m0 = M[k];
-    if (dx == 0.0) return m0;
-    const double slope = xmul(xsub(M[k + 1], m0), g.inv_w);
-    return xadd(xmul(slope, dx), m0);
+    if (dxw == 0.0) return m0;
+    return xadd(xmul(xsub(M[k + 1], m0), dxw), m0);
 }
 
 // DecodeStepLUT.lookup (costmodel.py:157-187) on the full power-of-two grid.
@@ -122,16 +130,16 @@ __device__ __forceinline__ double llookup(const Arr<double, WL>& M, const LGeo& 
     int c = (seq >> g.wsh) - 1;
     const bool in = seq > w && c < g.ns - 1;
     c = in ? c : (seq <= w ? 0 : g.ns - 1);
-    const double dx = in ? (double)(seq & (w - 1)) : 0.0;
+    const double dxw = in ? (double)(seq & (w - 1)) * g.inv_w : 0.0;
     // row selection (lut_rows_nb<true>)
     const int i = gbidx(bsz);
     const bool single = (i == 0) | (i >= g.nb) | ((1u << i) == (unsigned)bsz);
     const int lo = i >= g.nb ? g.nb - 1 : (i == 0 ? 0 : i - 1);
     const int r1 = single ? (i >= g.nb ? g.nb - 1 : i) : lo;
-    const double v1 = lrow(M, g, r1, c, dx);
+    const double v1 = lrow(M, g, r1, c, dxw);
     if (single) return v1;
-    const double v2 = lrow(M, g, i, c, dx);
-    return xadd(v1, xmul(xmul(xsub(v2, v1), (double)(bsz - (1 << lo))), pow2_neg(lo)));
+    const double v2 = lrow(M, g, i, c, dxw);
+    return xadd(v1, xmul(xsub(v2, v1), (double)(bsz - (1 << lo)) * pow2_neg(lo)));
 }
 
 // llookup with a one-entry memo: within one Alg. 3 scan the LUT is fixed, and consecutive candidates
@@ -142,7 +150,7 @@ __device__ __forceinline__ double llookup_memo(const Arr<double, WL>& M, const L
     int c = (seq >> g.wsh) - 1;
     const bool in = seq > w && c < g.ns - 1;
     c = in ? c : (seq <= w ? 0 : g.ns - 1);
-    const double dx = in ? (double)(seq & (w - 1)) : 0.0;
+    const double dx = in ? (double)(seq & (w - 1)) * g.inv_w : 0.0;
     if (bsz == mm.bsz && c == mm.c && dx == mm.dx) return mm.v;
     const int i = gbidx(bsz);
     const bool single = (i == 0) | (i >= g.nb) | ((1u << i) == (unsigned)bsz);
@@ -151,7 +159,7 @@ __device__ __forceinline__ double llookup_memo(const Arr<double, WL>& M, const L
     double v = lrow(M, g, r1, c, dx);
     if (!single) {
         const double v2 = lrow(M, g, i, c, dx);
-        v = xadd(v, xmul(xmul(xsub(v2, v), (double)(bsz - (1 << lo))), pow2_neg(lo)));
+        v = xadd(v, xmul(xsub(v2, v), (double)(bsz - (1 << lo)) * pow2_neg(lo)));
     }
     mm = LMemo{bsz, c, dx, v};
     return v;
@@ -451,8 +459,6 @@ __device__ __forceinline__ void ladmit(St& S, const LCtx& cx, const LWs& w) {
     const int32_t* Tout = cx.B.traces.output_len + S.off;
     const auto PR = w.r64(PD_TTR);
     const auto PP = w.r32(PD_POS), PI = w.r32(PD_IDR);
-    const auto AP = w.a32(A_POS), AS = w.a32(A_SEQ), AI = w.a32(A_IDR), AO = w.a32(A_OUT), AN = w.a32(A_INP),
-               AM = w.a32(A_MISS), AF = w.a32(A_FLAG);
     const auto AT = w.a64(A_TF);
     const int64_t kv_cap = linst(cx, S).kv_capacity_tokens;
     while (S.pt > S.ph) {
@@ -475,34 +481,26 @@ __device__ __forceinline__ void ladmit(St& S, const LCtx& cx, const LWs& w) {
         // kairos: keep the active set in (seq_len, id) order (decode_sched.py:74)
         int k = S.an;
         if (S.dpol == SLOSIM_DECODE_KAIROS_SLACK) {
-#ifndef SLOSIM_LANE_NO_PREFETCH_ADMIT
-            // shift the entries that sort after the new one up by one; entry k-2 is loaded while
-            // entry k-1 is stored at k
+            // shift the entries that sort after the new one up by one (three loads and stores per
+            // entry); entry k-2 is loaded while entry k-1 is stored at k
+            int4* V0 = w.v0();
+            int4* V1 = w.v1();
             if (k > 0) {
-                int32_t s_ = AS[k - 1], i_ = AI[k - 1], p_ = AP[k - 1], o_ = AO[k - 1], n_ = AN[k - 1],
-                        m_ = AM[k - 1], f_ = AF[k - 1];
+                int4 a_ = V0[(k - 1) * WL], b_ = V1[(k - 1) * WL];
                 int64_t t_ = AT[k - 1];
-                while (k > 0 && (s_ > inp || (s_ == inp && i_ > idr))) {
-                    int32_t s2 = 0, i2 = 0, p2 = 0, o2 = 0, n2 = 0, m2 = 0, f2 = 0;
+                while (k > 0 && (a_.x > inp || (a_.x == inp && a_.z > idr))) {
+                    int4 a2 = make_int4(0, 0, 0, 0), b2 = make_int4(0, 0, 0, 0);
                     int64_t t2 = 0;
-                    if (k > 1) {
-                        s2 = AS[k - 2]; i2 = AI[k - 2]; p2 = AP[k - 2]; o2 = AO[k - 2]; n2 = AN[k - 2];
-                        m2 = AM[k - 2]; f2 = AF[k - 2]; t2 = AT[k - 2];
-                    }
-                    AP[k] = p_; AS[k] = s_; AI[k] = i_; AO[k] = o_; AN[k] = n_; AM[k] = m_; AF[k] = f_; AT[k] = t_;
-                    s_ = s2; i_ = i2; p_ = p2; o_ = o2; n_ = n2; m_ = m2; f_ = f2; t_ = t2;
+                    if (k > 1) { a2 = V0[(k - 2) * WL]; b2 = V1[(k - 2) * WL]; t2 = AT[k - 2]; }
+                    V0[k * WL] = a_; V1[k * WL] = b_; AT[k] = t_;
+                    a_ = a2; b_ = b2; t_ = t2;
                     k--;
                 }
             }
-#else
-            while (k > 0 && (AS[k - 1] > inp || (AS[k - 1] == inp && AI[k - 1] > idr))) {
-                AP[k] = AP[k - 1]; AS[k] = AS[k - 1]; AI[k] = AI[k - 1]; AO[k] = AO[k - 1]; AN[k] = AN[k - 1];
-                AM[k] = AM[k - 1]; AF[k] = AF[k - 1]; AT[k] = AT[k - 1];
-                k--;
-            }
-#endif
         }
-        AP[k] = pos; AS[k] = inp; AI[k] = idr; AO[k] = outl; AN[k] = inp; AM[k] = 0; AF[k] = ttm ? 2 : 0; AT[k] = ttr;
+        w.v0()[k * WL] = make_int4(inp, ttm ? 2 : 0, idr, pos);
+        w.v1()[k * WL] = make_int4(inp, outl, 0, 0);
+        AT[k] = ttr;
 #ifndef SLOSIM_LANE_NO_VBASE
         S.vbase = min(S.vbase, ttr + S.tpot_slo);
 #endif
@@ -639,23 +637,19 @@ __device__ __forceinline__ void ldecode_done(St& S, const LWs& w, int64_t t) {
     int32_t pseq = -1, pidr = -1;
 #ifndef SLOSIM_LANE_NO_PREFETCH
     // software-pipelined: entry k+1 is loaded while entry k is processed (stores go to o <= k)
-    int32_t n_seq = 0, n_fl = 0, n_idr = 0, n_pos = 0, n_inp = 0, n_out = 0, n_miss = 0;
+    int4* const V0 = w.v0();
+    int4* const V1 = w.v1();
+    int4 na = make_int4(0, 0, 0, 0), nb = make_int4(0, 0, 0, 0);
     int64_t n_tf = 0;
-    if (an > 0) {
-        n_seq = AS[0]; n_fl = AF[0]; n_idr = AI[0]; n_pos = AP[0]; n_inp = AN[0]; n_out = AO[0]; n_miss = AM[0];
-        n_tf = AT[0];
-    }
+    if (an > 0) { na = V0[0]; nb = V1[0]; n_tf = AT[0]; }
 #ifndef SLOSIM_LANE_NO_VBASE
     int64_t vb = SLOSIM_INF64;
 #endif
     for (int k = 0; k < an; k++) {
-        int32_t seq = n_seq;
-        const int32_t fl = n_fl, idr = n_idr, pos = n_pos, inp = n_inp, outl = n_out, miss0 = n_miss;
+        int32_t seq = na.x;
+        const int32_t fl = na.y, idr = na.z, pos = na.w, inp = nb.x, outl = nb.y, miss0 = nb.z;
         const int64_t tf = n_tf;
-        if (k + 1 < an) {
-            n_seq = AS[k + 1]; n_fl = AF[k + 1]; n_idr = AI[k + 1]; n_pos = AP[k + 1]; n_inp = AN[k + 1];
-            n_out = AO[k + 1]; n_miss = AM[k + 1]; n_tf = AT[k + 1];
-        }
+        if (k + 1 < an) { na = V0[(k + 1) * WL]; nb = V1[(k + 1) * WL]; n_tf = AT[k + 1]; }
         if (pre >= 0 ? k < pre : (fl & 1)) {
             seq += 1;
             const int ngen = seq - inp;
@@ -678,17 +672,22 @@ __device__ __forceinline__ void ldecode_done(St& S, const LWs& w, int64_t t) {
                 kv_rel += (int64_t)inp + outl;
                 continue;
             }
-            if (o != k) { AP[o] = pos; AN[o] = inp; AO[o] = outl; AT[o] = tf; AI[o] = idr; }
-            AM[o] = miss;
-            AS[o] = seq;
-            AF[o] = fl & ~1;
+            if (o != k) {
+                V0[o * WL] = make_int4(seq, fl & ~1, idr, pos);
+                V1[o * WL] = make_int4(inp, outl, miss, 0);
+                AT[o] = tf;
+            } else {
+                *(int2*)&V0[o * WL] = make_int2(seq, fl & ~1);
+                AM[o] = miss;
+            }
         } else {
 #ifndef SLOSIM_LANE_NO_VBASE
             if (kairos) vb = min(vb, tf + ((int64_t)(seq - inp) + 1) * S.tpot_slo);
 #endif
             if (o != k) {
-                AP[o] = pos; AN[o] = inp; AO[o] = outl; AT[o] = tf; AI[o] = idr; AM[o] = miss0; AS[o] = seq;
-                AF[o] = fl;
+                V0[o * WL] = make_int4(seq, fl, idr, pos);
+                V1[o * WL] = make_int4(inp, outl, miss0, 0);
+                AT[o] = tf;
             }
         }
         if (kairos) moved |= seq < pseq || (seq == pseq && idr < pidr);
@@ -745,18 +744,19 @@ __device__ __forceinline__ void ldecode_done(St& S, const LWs& w, int64_t t) {
 #endif
     if (moved) {
         // members moved up by one token: restore (seq_len, id) order by insertion
+        int4* const V0 = w.v0();
+        int4* const V1 = w.v1();
         for (int k = 1; k < o; k++) {
-            const int32_t sk = AS[k], ik = AI[k];
-            if (!(AS[k - 1] > sk || (AS[k - 1] == sk && AI[k - 1] > ik))) continue;
-            const int32_t p = AP[k], n_ = AN[k], ou = AO[k], mi = AM[k], fl = AF[k];
+            const int4 a = V0[k * WL];
+            if (!(AS[k - 1] > a.x || (AS[k - 1] == a.x && AI[k - 1] > a.z))) continue;
+            const int4 b = V1[k * WL];
             const int64_t tf = AT[k];
             int j = k;
-            while (j > 0 && (AS[j - 1] > sk || (AS[j - 1] == sk && AI[j - 1] > ik))) {
-                AP[j] = AP[j - 1]; AS[j] = AS[j - 1]; AI[j] = AI[j - 1]; AO[j] = AO[j - 1]; AN[j] = AN[j - 1];
-                AM[j] = AM[j - 1]; AF[j] = AF[j - 1]; AT[j] = AT[j - 1];
+            while (j > 0 && (AS[j - 1] > a.x || (AS[j - 1] == a.x && AI[j - 1] > a.z))) {
+                V0[j * WL] = V0[(j - 1) * WL]; V1[j * WL] = V1[(j - 1) * WL]; AT[j] = AT[j - 1];
                 j--;
             }
-            AP[j] = p; AS[j] = sk; AI[j] = ik; AO[j] = ou; AN[j] = n_; AM[j] = mi; AF[j] = fl; AT[j] = tf;
+            V0[j * WL] = a; V1[j * WL] = b; AT[j] = tf;
         }
     }
     if (S.use_lut) {
@@ -809,11 +809,12 @@ __device__ __forceinline__ void ldecode_start(St& S, const LWs& w, int64_t t) {
             double tcur = 0.0;
             LMemo mm{-1, -1, 0.0, 0.0};
 #ifndef SLOSIM_LANE_NO_SCAN_FLAGS
-            // candidate k+1's key and flag word are loaded while candidate k is decided
-            int nseq = AS[0], nfl = AF[0];
+            // candidate k+1's key and flag word (one 8-byte load) are loaded while candidate k is decided
+            const int2* const V0 = (const int2*)w.v0();
+            int2 nv = V0[0];
             for (int k = 0; k < an; k++) {
-                const int seq = nseq, fl = nfl;
-                if (k + 1 < an) { nseq = AS[k + 1]; nfl = AF[k + 1]; }
+                const int seq = nv.x, fl = nv.y;
+                if (k + 1 < an) nv = V0[(k + 1) * WL * 2];
                 const double ts = llookup_memo(M, g, b + 1, seq, mm);
                 if (ts <= smin && (b == 0 || lquot_gt((double)(b + 1), ts, (double)b, tcur))) {
                     AF[k] = fl | 1;

@@ -53,3 +53,9 @@ static inline unsigned long long atomicAdd(unsigned long long* p, unsigned long 
 template <class T> static inline T __shfl_up_sync(unsigned, T, int) { hc_no_warp(); }
 static inline int __reduce_min_sync(unsigned, int) { hc_no_warp(); }
 static inline int __all_sync(unsigned, int) { hc_no_warp(); }
+
+// CUDA's vector types (the lane engine's active-set entries)
+struct alignas(16) int4 { int x, y, z, w; };
+struct alignas(8) int2 { int x, y; };
+static inline int4 make_int4(int x, int y, int z, int w) { return int4{x, y, z, w}; }
+static inline int2 make_int2(int x, int y) { return int2{x, y}; }
