@@ -1082,14 +1082,14 @@ __device__ __forceinline__ double ff_row(const double* M, const Geo& g, double i
     const double a = k == c0 ? m0 : M[k];
     if (cs.dx == 0.0) return a;
     const double b = k + 1 == c0 ? m0 : M[k + 1];
-    return xadd(xmul(xmul(xsub(b, a), inv_w), cs.dx), a);
+    return xadd(xmul(xsub(b, a), cs.dx * inv_w), a);  // = slope * dx, slope = (b - a) * 2^-wsh (exact scaling)
 }
 __device__ __forceinline__ double ff_lookup(const LutMem* L, const Geo& g, double inv_w, const RowP& rp, int seq,
                                             int c0, double m0) {
     const ColSel cs = gcol(g, seq);
     const double v1 = ff_row(L->mean, g, inv_w, rp.r1, cs, c0, m0);
     const double v2 = rp.r2 == rp.r1 ? v1 : ff_row(L->mean, g, inv_w, rp.r2, cs, c0, m0);
-    return xadd(v1, xmul(xmul(xsub(v2, v1), (double)rp.num), rp.inv));
+    return xadd(v1, xmul(xsub(v2, v1), rp.wgt));
 }
 __device__ __forceinline__ bool ff_quot_gt(double a, double x, double b, double y) {
     bool tie;
@@ -1098,79 +1098,49 @@ __device__ __forceinline__ bool ff_quot_gt(double a, double x, double b, double 
 }
 
 // ff_steps<.., V = true>: lane k verifies that the step started at e_k (after completions 0..k of
-// the run, each of them batching the same set B of the active set A) batches B again.  `e` is this
-// lane's e_k; `rank` the lane's (seq_len, id) rank among A at time t (scan_geo's cache).
+// the run, each of them batching the whole active set A) batches A again.  `e` is this lane's e_k;
+// `rank` the lane's (seq_len, id) rank among A at time t (scan_geo's cache).
 __device__ __noinline__ bool ff_verify(const Sim& S, const Slot& sl, int64_t t, int64_t e, int lane, const RowP* rowtab,
                                        int rank) {
     const bool occ = (S.amask >> lane) & 1u;
-    const bool mem = (S.dc_mask >> lane) & 1u;
-    const int an = S.an, nb = __popc(S.dc_mask), nn = an - nb;
+    const int an = S.an;
     const int64_t tpot = S.tpot_slo;
-    // B's and A\B's (seq_len, id) keys, each in rank order (per-warp shared memory): members advance
-    // one token per step and keep their relative order, the others keep theirs, so the order at
-    // step k+1 is the merge of the two lists with B's lengths advanced by k+1
-    __shared__ int32_t ff_flag[4][32];
-    __shared__ int32_t ff_key[4][2][2][32];  // [list: B, A\B][seq, id][index]
-    const int wib = threadIdx.x >> 5;
+    // the active set's sequence lengths in rank order (per-warp shared memory)
+    __shared__ int32_t ff_seq[4][32];
+    int32_t* rs = ff_seq[threadIdx.x >> 5];
     __syncwarp();
-    if (occ) ff_flag[wib][rank] = mem;
-    __syncwarp();
-    const unsigned mrank = __ballot_sync(FULLMASK, lane < an && ff_flag[wib][lane]);  // members by rank
-    if (occ) {
-        const int below = __popc(mrank & ((1u << rank) - 1u));
-        const int li = mem ? 0 : 1, idx = mem ? below : rank - below;
-        ff_key[wib][li][0][idx] = sl.seq;
-        ff_key[wib][li][1][idx] = sl.idr;
-    }
-    // slack (decode_sched.py:36-57) at step k+1: tpot*(n_gen + 1 [+ k+1 for members]) - (e_k - t_first)
-    const int64_t vb = occ ? tpot * ((int64_t)(sl.seq - sl.inp) + 1) + sl.tf : SLOSIM_INF64;
-    const int64_t vmb = wmin64_redux(mem ? vb : SLOSIM_INF64);
-    const int64_t vmn = wmin64_redux(occ && !mem ? vb : SLOSIM_INF64);
-    const int mxn = __reduce_max_sync(FULLMASK, occ && !mem ? sl.seq : 0);
+    if (occ) rs[rank] = sl.seq;
+    // slack (decode_sched.py:36-57) at step k+1: tpot*(n_gen + k + 2) - (e_k - t_first)
+    const int64_t v0 = wmin64_redux(occ ? tpot * ((int64_t)(sl.seq - sl.inp) + 1) + sl.tf : SLOSIM_INF64);
     __syncwarp();
     const LutMem* L = S.L;
     const Geo g = geo_of(L);
     const double inv_w = pow2_neg(g.wsh);
     const int kk = lane + 1;  // completions applied before step k+1 starts
     // cell c0 after kk completions: exact integer sum (checked integral by the caller's commit) over count
-    const int i0 = min(gbidx(nb), g.nb - 1);
+    const int i0 = min(gbidx(an), g.nb - 1);
     const int j0 = min((int)((S.dc_max + (1 << g.wsh) - 1) >> g.wsh) - 1, g.ns - 1);
     const int c0 = i0 * g.ns + j0;
     const double s0 = L->sum[c0];
     if (!(s0 == rint(s0) && fabs(s0) + (double)(e - t) < 0x1p53)) return false;
     const double m0 = xdiv(xadd(s0, (double)(e - t)), (double)(L->cnt[c0] + kk));
-    int64_t vmin = vmb + (int64_t)kk * tpot;
-    vmin = (vmn < vmin ? vmn : vmin) - e;
-    const int amax = max((int)S.dc_max + kk, mxn);
-    const double fb = ff_lookup(L, g, inv_w, rowtab[an], amax, c0, m0);
+    const int64_t vmin = v0 + (int64_t)kk * tpot - e;
+    const double fb = ff_lookup(L, g, inv_w, rowtab[an], (int)S.amax + kk, c0, m0);
     const double smin = xsub((double)vmin, fb);
-    // the greedy scan in merged (seq_len, id) order must admit exactly the members
-    const int32_t* bs = ff_key[wib][0][0];
-    const int32_t* bi = ff_key[wib][0][1];
-    const int32_t* ns_ = ff_key[wib][1][0];
-    const int32_t* ni = ff_key[wib][1][1];
-    int ib = 0, in_ = 0, b = 0;
-    double tcur = 0.0;
-    bool ok = true;
+    // greedy scan admitting every candidate in (seq_len, id) order
+    bool all = true;
+    double xp = 0.0;
 #pragma unroll 1
     for (int r = 0; r < an; r++) {
-        bool take_b = in_ >= nn;
-        if (!take_b && ib < nb) {
-            const int sb = bs[ib] + kk, sn = ns_[in_];
-            take_b = sb < sn || (sb == sn && bi[ib] < ni[in_]);
-        }
-        const int seq = take_b ? bs[ib] + kk : ns_[in_];
-        if (take_b) ib++; else in_++;
-        const double x = ff_lookup(L, g, inv_w, rowtab[b + 1], seq, c0, m0);
-        const bool adm = x <= smin && (b == 0 || ff_quot_gt((double)(b + 1), x, (double)b, tcur));
-        if (adm != take_b) { ok = false; break; }
-        if (adm) { b++; tcur = x; }
+        const double x = ff_lookup(L, g, inv_w, rowtab[r + 1], rs[r] + kk, c0, m0);
+        if (!(x <= smin && (r == 0 || ff_quot_gt((double)(r + 1), x, (double)r, xp)))) { all = false; break; }
+        xp = x;
     }
-    if (ok || nn > 0) return ok;
-    // B = A: or admitting none (every candidate rejected against the empty batch), the fallback
+    if (all) return true;
+    // or admitting none (every candidate rejected against the empty batch): the fallback batches A
 #pragma unroll 1
     for (int r = 0; r < an; r++)
-        if (ff_lookup(L, g, inv_w, rowtab[1], bs[r] + kk, c0, m0) <= smin) return false;
+        if (ff_lookup(L, g, inv_w, rowtab[1], rs[r] + kk, c0, m0) <= smin) return false;
     return true;
 }
 
@@ -1193,24 +1163,24 @@ __device__ __noinline__ bool ff_verify(const Sim& S, const Slot& sl, int64_t t, 
 // is left in progress exactly as the loop would have started it.  Returns m.
 // Preconditions (checked by the caller): register mode, plain formula ground
 // truth, no per-step trace, no pending prefill start; LUTUPD: a fully
-// populated LUT and either one active request or (V) any batch B of the
-// active set A.
+// populated LUT and either one active request or (V) a batch that is the whole
+// active set.
 //
-// V (Alg. 3 with |A| > 1): the decision of every later step in the run is
-// verified instead of assumed.  Lane k re-runs select_decode_batch
-// (decode_sched.py:60-111) for step k+1 as the loop would see it at time e_k:
-// the members of B advanced by k+1 tokens and the others not (the order is the
-// merge of the two rank-ordered lists), the slack minima of both shifted
-// accordingly, and the LUT as the k+1 earlier completions leave it (only cell
-// c0 differs: its exact integer sum over its count; lookups read means and
-// form the np.interp slopes as the stored slopes are formed).  The step batches
-// B again iff the greedy scan admits exactly B's members, or (B = A) none of
-// them (the fallback).  The run is the leading prefix of steps whose completion
-// is pure and whose successor's decision is verified.
+// V (Alg. 3 with |A| > 1, the step just started batching all of A): the
+// decision of every later step in the run is verified instead of assumed.
+// Lane k re-runs select_decode_batch (decode_sched.py:60-111) for step k+1 as
+// the loop would see it at time e_k: every request advanced by k+1 tokens (so
+// the (seq_len, id) order is unchanged), the slack minimum shifted by
+// (k+1)*tpot - (e_k - t), and the LUT as the k+1 earlier completions leave it
+// (only cell c0 differs: its exact integer sum over its count; lookups read
+// means and form the np.interp slopes as the stored slopes are formed).  The
+// step batches A again iff the greedy scan admits every candidate, or none
+// (the fallback).  The run is the leading prefix of steps whose completion is
+// pure and whose successor's decision is verified.
 template <bool LUTUPD, bool G, bool V = false>
 __device__ __noinline__ int ff_steps(Sim& S, Slot& sl, int64_t t, int lane, const RowP* rowtab = nullptr,
                                      int rank = 0) {
-    const bool occ = (S.dc_mask >> lane) & 1u;  // a member of the running batch
+    const bool occ = (S.amask >> lane) & 1u;  // every active request is in the batch
     const int64_t ng = (int64_t)sl.seq - sl.inp;  // tokens generated before step 0
     const int r = __reduce_min_sync(FULLMASK, occ ? (int)(sl.out - 2 - ng) : 0x7fffffff);
     if (r < 1) return 0;
@@ -1272,7 +1242,7 @@ __device__ __noinline__ int ff_steps(Sim& S, Slot& sl, int64_t t, int lane, cons
     S.dc_end = __shfl_sync(FULLMASK, e, m);
     S.dc_dur = __shfl_sync(FULLMASK, d, m);
     S.dc_max = bmax + m;
-    S.amax = __reduce_max_sync(FULLMASK, ((S.amask >> lane) & 1u) ? sl.seq : 0);
+    S.amax += m;
     return m;
 }
 
@@ -1606,10 +1576,10 @@ __device__ SIM_INLINE void simulate(const Ctx& cx, int64_t ii, const WS& w, int 
 #ifndef SLOSIM_NO_FF
             // Alg. 3 runs that repeat a batch (|A| > 1) are verified step by step (ff_steps<.., V>);
             // the geometry scan keeps the ranks they need
-            // when the step batches the whole active set: repeated partial batches verify too
-            // (ff_verify is general) but fail too often to pay for the attempts (config 2: 5.72 s
-            // with whole-set runs only, 6.10 s with partial batches the previous step also ran,
-            // 6.93 s with every batch)
+            // when the step batches the whole active set (a verifier for repeated partial batches,
+            // merging the advanced members into the others' order, was exact but slower: config 2
+            // 5.72 s with whole-set runs only, 6.10 s with partial batches the previous step also
+            // ran, 6.93 s with every batch, 6.04 s general verifier on whole-set runs)
             const bool ff_multi = DP == SLOSIM_DECODE_KAIROS_SLACK && FF_MULTI && G && an > 1 && bsz == an;
             if ((DP == SLOSIM_DECODE_CONTINUOUS ? !use_lut : (FF_KAIROS && (an == 1 || ff_multi))) &&
                 (DP == SLOSIM_DECODE_CONTINUOUS || lut_full) && regmode && gt_plain && !(FULL && S.T.buf) &&

@@ -252,7 +252,8 @@ __device__ __forceinline__ double lut_eval(const LutMem* L, const RowSel& rs, co
     int k2 = rs.r2 * ns + cs.c;
     double v2 = xadd(xmul(L->slope[k2], cs.dx), L->mean[k2]);
     // v_lo + (v_hi - v_lo) * (bsz - b_lo) / (b_hi - b_lo)
-    if (G) return xadd(v1, xmul(xmul(xsub(v2, v1), (double)rs.num), rs.inv));
+    // (power-of-two weights: RN(RN(d * num) * 2^-lo) = RN(d * (num * 2^-lo)), one multiply)
+    if (G) return xadd(v1, xmul(xsub(v2, v1), (double)rs.num * rs.inv));
     return xadd(v1, xdiv(xmul(xsub(v2, v1), (double)rs.num), (double)rs.den));
 }
 
@@ -290,7 +291,7 @@ __device__ __forceinline__ double geval(const LutMem* L, const Geo& g, const Row
     const int k2 = (rs.r2 < 0 ? rs.r1 : rs.r2) * g.ns + cs.c;
     const double v1 = xadd(xmul(L->slope[k1], cs.dx), L->mean[k1]);
     const double v2 = xadd(xmul(L->slope[k2], cs.dx), L->mean[k2]);
-    const double r = xadd(v1, xmul(xmul(xsub(v2, v1), (double)rs.num), rs.inv));
+    const double r = xadd(v1, xmul(xsub(v2, v1), (double)rs.num * rs.inv));
     return rs.r2 < 0 ? v1 : r;
 }
 
@@ -298,16 +299,16 @@ __device__ __forceinline__ double geval(const LutMem* L, const Geo& g, const Row
 // table: rows r1, r2 (r2 = r1 for a single row) and the Python-form weight
 // num * 2^-lo.  A single row then evaluates as v1 + (v1 - v1) * 0 = v1 exactly
 // (LUT means are positive), so the evaluation needs no select.
-struct RowP { int16_t r1, r2; int32_t num; double inv; };
+struct RowP { int16_t r1, r2; int32_t num; double wgt; };  // wgt = num * 2^-lo, exact
 __device__ __forceinline__ RowP rowp_of(const Geo& g, int bsz) {
     const RowSel rs = grows(g, bsz);
-    return RowP{(int16_t)rs.r1, (int16_t)(rs.r2 < 0 ? rs.r1 : rs.r2), (int32_t)rs.num, rs.inv};
+    return RowP{(int16_t)rs.r1, (int16_t)(rs.r2 < 0 ? rs.r1 : rs.r2), (int32_t)rs.num, (double)rs.num * rs.inv};
 }
 __device__ __forceinline__ double geval_p(const LutMem* L, const Geo& g, const RowP& rp, const ColSel& cs) {
     const int k1 = rp.r1 * g.ns + cs.c, k2 = rp.r2 * g.ns + cs.c;
     const double v1 = xadd(xmul(L->slope[k1], cs.dx), L->mean[k1]);
     const double v2 = xadd(xmul(L->slope[k2], cs.dx), L->mean[k2]);
-    return xadd(v1, xmul(xmul(xsub(v2, v1), (double)rp.num), rp.inv));
+    return xadd(v1, xmul(xsub(v2, v1), rp.wgt));
 }
 
 #ifdef __CUDACC__
