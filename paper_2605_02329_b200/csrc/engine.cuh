@@ -1097,11 +1097,13 @@ __device__ __forceinline__ bool ff_quot_gt(double a, double x, double b, double 
     return tie ? quot_gt_exact(a, x, b, y) : gt;
 }
 
-// ff_steps<.., V = true>: lane k verifies that the step started at e_k (after completions 0..k of
-// the run, each of them batching the whole active set A) batches A again.  `e` is this lane's e_k;
-// `rank` the lane's (seq_len, id) rank among A at time t (scan_geo's cache).
-__device__ __noinline__ bool ff_verify(const Sim& S, const Slot& sl, int64_t t, int64_t e, int lane, const RowP* rowtab,
-                                       int rank) {
+// ff_steps<.., V = true>: lane k runs select_decode_batch for the step started at e_k (after
+// completions 0..k of the run, each of them batching the whole active set A) and returns the batch
+// as a mask over A's (seq_len, id) ranks: all of A when the greedy scan admits every candidate or
+// none (the fallback), 0 when the run's LUT cell leaves the exact integer range.  `e` is this
+// lane's e_k; `rank` the lane's rank among A at time t (scan_geo's cache).
+__device__ __noinline__ uint32_t ff_verify(const Sim& S, const Slot& sl, int64_t t, int64_t e, int lane,
+                                           const RowP* rowtab, int rank) {
     const bool occ = (S.amask >> lane) & 1u;
     const int an = S.an;
     const int64_t tpot = S.tpot_slo;
@@ -1122,26 +1124,26 @@ __device__ __noinline__ bool ff_verify(const Sim& S, const Slot& sl, int64_t t, 
     const int j0 = min((int)((S.dc_max + (1 << g.wsh) - 1) >> g.wsh) - 1, g.ns - 1);
     const int c0 = i0 * g.ns + j0;
     const double s0 = L->sum[c0];
-    if (!(s0 == rint(s0) && fabs(s0) + (double)(e - t) < 0x1p53)) return false;
+    if (!(s0 == rint(s0) && fabs(s0) + (double)(e - t) < 0x1p53)) return 0u;
     const double m0 = xdiv(xadd(s0, (double)(e - t)), (double)(L->cnt[c0] + kk));
     const int64_t vmin = v0 + (int64_t)kk * tpot - e;
     const double fb = ff_lookup(L, g, inv_w, rowtab[an], (int)S.amax + kk, c0, m0);
     const double smin = xsub((double)vmin, fb);
-    // greedy scan admitting every candidate in (seq_len, id) order
-    bool all = true;
-    double xp = 0.0;
+    // the greedy scan in (seq_len, id) order (decode_sched.py:84-95)
+    const uint32_t full = an >= 32 ? ~0u : (1u << an) - 1u;
+    uint32_t adm = 0;
+    int b = 0;
+    double tcur = 0.0;
 #pragma unroll 1
     for (int r = 0; r < an; r++) {
-        const double x = ff_lookup(L, g, inv_w, rowtab[r + 1], rs[r] + kk, c0, m0);
-        if (!(x <= smin && (r == 0 || ff_quot_gt((double)(r + 1), x, (double)r, xp)))) { all = false; break; }
-        xp = x;
+        const double x = ff_lookup(L, g, inv_w, rowtab[b + 1], rs[r] + kk, c0, m0);
+        if (x <= smin && (b == 0 || ff_quot_gt((double)(b + 1), x, (double)b, tcur))) {
+            adm |= 1u << r;
+            b++;
+            tcur = x;
+        }
     }
-    if (all) return true;
-    // or admitting none (every candidate rejected against the empty batch): the fallback batches A
-#pragma unroll 1
-    for (int r = 0; r < an; r++)
-        if (ff_lookup(L, g, inv_w, rowtab[1], rs[r] + kk, c0, m0) <= smin) return false;
-    return true;
+    return b == 0 ? full : adm;  // nothing admitted: the fallback decodes all of A
 }
 
 // Decode steps between rare events, applied in bulk.  Under continuous
@@ -1202,14 +1204,23 @@ __device__ __noinline__ int ff_steps(Sim& S, Slot& sl, int64_t t, int lane, cons
         const int j0 = __shfl_sync(FULLMASK, j, 0);  // unconditional: every lane takes part
         pure = pure && j == j0;
     }
+    uint32_t vmask = 0;
+    bool tail = false;
+    int m;
     if (V) {  // every lane takes part in the verification's collectives
-        const bool vf = ff_verify(S, sl, t, e, lane, rowtab, rank);
-        pure = pure && vf;
+        vmask = ff_verify(S, sl, t, e, lane, rowtab, rank);
+        const uint32_t full = S.an >= 32 ? ~0u : (1u << S.an) - 1u;
+        // the leading run of verified steps; when the step after it batches a proper subset of A
+        // and the run's last completion is pure, that step is started here too (the tail)
+        const unsigned pm = __ballot_sync(FULLMASK, pure && vmask == full);
+        m = __ffs((int)~pm) - 1;
+        tail = __shfl_sync(FULLMASK, pure && vmask != 0u && vmask != full, m & 31) && m < 31;
+        vmask = __shfl_sync(FULLMASK, vmask, m & 31);
+        m += tail ? 1 : 0;
+    } else {
+        // end times increase and the other bounds are thresholds, so the pure steps form a prefix
+        m = __popc(__ballot_sync(FULLMASK, pure));
     }
-    // end times increase and the other bounds are thresholds, so the pure steps form a prefix
-    // (V: the leading run of verified steps)
-    const unsigned pm = __ballot_sync(FULLMASK, pure);
-    const int m = V ? __ffs((int)~pm) - 1 : __popc(pm);
     if (m <= 0) return 0;
     if (LUTUPD) {
         const int64_t dsum = wsum64(lane < m ? d : 0);
@@ -1239,10 +1250,24 @@ __device__ __noinline__ int ff_steps(Sim& S, Slot& sl, int64_t t, int lane, cons
     }
     if (occ) { sl.seq += m; sl.miss += miss; }
     S.D = D;
+    S.amax += m;
+    if (V && tail) {
+        // step m batches the ranks in vmask: membership, its max_seq and ground-truth duration
+        const bool in = occ && ((vmask >> rank) & 1u);
+        S.dc_mask = __ballot_sync(FULLMASK, in);
+        const int tb = __popc(vmask);
+        const int tmax = __reduce_max_sync(FULLMASK, in ? sl.seq : 0);
+        int64_t td = rint_i64(decode_formula(P->n_base, P->base_x, P->base_y, P->gamma, tb, tmax));
+        td = td < 1 ? 1 : td;
+        S.dc_end = __shfl_sync(FULLMASK, e, m - 1) + td;
+        S.dc_dur = td;
+        S.dc_bsz = tb;
+        S.dc_max = tmax;
+        return m;
+    }
     S.dc_end = __shfl_sync(FULLMASK, e, m);
     S.dc_dur = __shfl_sync(FULLMASK, d, m);
     S.dc_max = bmax + m;
-    S.amax += m;
     return m;
 }
 
@@ -1597,7 +1622,8 @@ __device__ SIM_INLINE void simulate(const Ctx& cx, int64_t ii, const WS& w, int 
                 PROF_COUNT(9, m);
                 dsteps += m;
                 v_dec += (int64_t)m * an;
-                b_dec += (int64_t)m * bsz;
+                // the run's last step may batch a subset of A (ff_steps<.., V> tail): dc_bsz
+                b_dec += m > 0 ? (int64_t)(m - 1) * bsz + dc_bsz : 0;
             }
 #endif
         }

@@ -906,6 +906,13 @@ __device__ __forceinline__ bool lstep(St& S, const LCtx& cx, const LWs& w) {
 #define SLOSIM_LANE_MIN_BLOCKS 2
 #endif
 
+// Urgency/SJF prefill starts over a queue of at most this many requests run on the lane itself
+// (quadratic in the queue length, but every such lane proceeds at once); longer queues go to the
+// warp-cooperative path
+#ifndef SLOSIM_LANE_SERIAL_PF_MAX
+#define SLOSIM_LANE_SERIAL_PF_MAX 8
+#endif
+
 // Persistent lane engine: each lane pulls instances (in `order`) from the work counter.
 __global__ void __launch_bounds__(128, SLOSIM_LANE_MIN_BLOCKS)
     lane_kernel(const __grid_constant__ LCtx cx, char* ws_base, int64_t cap, int cells, unsigned long long* work,
@@ -945,7 +952,7 @@ __global__ void __launch_bounds__(128, SLOSIM_LANE_MIN_BLOCKS)
         if (live) live = lstep_a(S, cx, w, t, need_pf);
         // prefill starts: FCFS packs a prefix of the queue, cheap on the lane itself; the urgency and
         // SJF policies order the whole queue, so one lane's queue at a time, all lanes cooperating
-        if (need_pf && S.ppol == SLOSIM_PREFILL_FCFS) {
+        if (need_pf && (S.ppol == SLOSIM_PREFILL_FCFS || S.qt - S.qh <= SLOSIM_LANE_SERIAL_PF_MAX)) {
             lprefill_start(S, cx, w, t);
             need_pf = false;
         }
