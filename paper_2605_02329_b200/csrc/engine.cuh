@@ -1281,6 +1281,10 @@ __device__ __noinline__ int ff_steps(Sim& S, Slot& sl, int64_t t, int lane, cons
 #define FF_MULTI true
 #endif
 
+#ifndef FF_MIN_STREAK
+#define FF_MIN_STREAK 3
+#endif
+
 #ifdef SLOSIM_NO_FF_KAIROS
 #define FF_KAIROS false
 #else
@@ -1370,6 +1374,7 @@ __device__ SIM_INLINE void simulate(const Ctx& cx, int64_t ii, const WS& w, int 
     bool lut_full = use_lut && L->full != 0;
     int rk_rank = 0, rk_pred = lane;  // cached slot ranks of the kairos scan (scan_geo)
     uint32_t rk_mask = 0;
+    int ff_streak = 0;
     const Geo geo = G ? geo_of(ST) : Geo{0, 0, 0};
     // row selections of batch sizes 1..32 for the register-mode scan (per warp)
     __shared__ RowP row_tabs[4][33];
@@ -1605,7 +1610,13 @@ __device__ SIM_INLINE void simulate(const Ctx& cx, int64_t ii, const WS& w, int 
             // merging the advanced members into the others' order, was exact but slower: config 2
             // 5.72 s with whole-set runs only, 6.10 s with partial batches the previous step also
             // ran, 6.93 s with every batch, 6.04 s general verifier on whole-set runs)
-            const bool ff_multi = DP == SLOSIM_DECODE_KAIROS_SLACK && FF_MULTI && G && an > 1 && bsz == an;
+            // and the steps before it did too (ff_streak: consecutive steps batching the whole active
+            // set, FF_MIN_STREAK of them before an attempt): an attempt whose first step fails costs
+            // about one step, and a partial batch tends to follow a partial batch
+            const bool whole = bsz == an;
+            const bool ff_multi = DP == SLOSIM_DECODE_KAIROS_SLACK && FF_MULTI && G && an > 1 && whole &&
+                                  ff_streak >= FF_MIN_STREAK;
+            ff_streak = whole ? ff_streak + 1 : 0;
             if ((DP == SLOSIM_DECODE_CONTINUOUS ? !use_lut : (FF_KAIROS && (an == 1 || ff_multi))) &&
                 (DP == SLOSIM_DECODE_CONTINUOUS || lut_full) && regmode && gt_plain && !(FULL && S.T.buf) &&
                 dc_end < t_rare && !pf_wait) {
@@ -1622,6 +1633,7 @@ __device__ SIM_INLINE void simulate(const Ctx& cx, int64_t ii, const WS& w, int 
                 PROF_COUNT(9, m);
                 dsteps += m;
                 v_dec += (int64_t)m * an;
+                ff_streak = dc_bsz == bsz ? ff_streak + m : 0;  // a trailing partial step ends the streak
                 // the run's last step may batch a subset of A (ff_steps<.., V> tail): dc_bsz
                 b_dec += m > 0 ? (int64_t)(m - 1) * bsz + dc_bsz : 0;
             }
