@@ -1275,7 +1275,7 @@ __device__ __noinline__ int ff_steps(Sim& S, Slot& sl, int64_t t, int lane, cons
 // build the other resident warps use the issue slots a failed verification costs (configs 3 and 4:
 // 213 -> 265 ms and 685 -> 1045 ms with it), in the latency build nothing else would (config 2:
 // 6.78 -> 5.73 s, config 1: 83 -> 66 ms).
-#if defined(SLOSIM_NO_FF_MULTI) || !defined(SLOSIM_MIN_BLOCKS) || SLOSIM_MIN_BLOCKS != 1
+#if defined(SLOSIM_NO_FF_MULTI) || ((!defined(SLOSIM_MIN_BLOCKS) || SLOSIM_MIN_BLOCKS != 1) && !defined(SLOSIM_FF_MULTI_ALL))
 #define FF_MULTI false
 #else
 #define FF_MULTI true
