@@ -947,7 +947,6 @@ __device__ __noinline__ bool quot_gt_exact(double a, double x, double b, double 
 // the occupied-lane set rk_mask) and reused when the slot set is unchanged and
 // every slot still compares above its rank predecessor: the old rank order is
 // then still sorted, so the ranks are unchanged.
-template <bool SERIAL = false>
 __device__ __forceinline__ int scan_geo(const LutMem* L, const Geo& g, const RowP* rowtab, uint32_t amask, int an,
                                         const Slot& sl, int64_t vmin, uint32_t& adm, int& mseq, int& rk_rank,
                                         int& rk_pred, uint32_t& rk_mask, int lane) {
@@ -973,35 +972,6 @@ __device__ __forceinline__ int scan_geo(const LutMem* L, const Geo& g, const Row
         rk_rank = rank;
         rk_pred = pred;
         rk_mask = amask;
-    }
-    if (SERIAL) {
-        // small active sets: every lane runs the greedy scan (decode_sched.py:84-95) over the
-        // rank-ordered lengths in shared memory, one candidate after another, with no collectives
-        // inside the scan (the same values on every lane, so the loop is uniform)
-        __shared__ int32_t ss_seq[4][32];
-        int32_t* rs = ss_seq[threadIdx.x >> 5];
-        __syncwarp();
-        if (occ) rs[rank] = sl.seq;
-        __syncwarp();
-        const double smin = xsub((double)vmin, geval_p(L, g, rowtab[an], gcol(g, rs[an - 1])));
-        uint32_t radm = 0;
-        int b = 0, ms = 0;
-        double tcur = 0.0;
-#pragma unroll 1
-        for (int r = 0; r < an; r++) {
-            const int sq = rs[r];
-            const double x = geval_p(L, g, rowtab[b + 1], gcol(g, sq));
-            bool ok = x <= smin;
-            if (ok && b != 0) {
-                bool tie;
-                ok = quot_gt_fast((double)(b + 1), x, (double)b, tcur, tie);
-                if (tie) ok = quot_gt_exact((double)(b + 1), x, (double)b, tcur);
-            }
-            if (ok) { radm |= 1u << r; b++; tcur = x; ms = sq; }
-        }
-        adm = __ballot_sync(FULLMASK, occ && ((radm >> rank) & 1u));
-        mseq = ms;
-        return b;
     }
     const ColSel cs = gcol(g, occ ? sl.seq : 1);
     int b = 0, s = 0;
@@ -1312,11 +1282,6 @@ __device__ __noinline__ int ff_steps(Sim& S, Slot& sl, int64_t t, int lane, cons
 #define FF_MULTI true
 #endif
 
-// Alg. 3 scans over at most this many active requests run serially on every lane (scan_geo<true>)
-#ifndef SCAN_SERIAL_MAX
-#define SCAN_SERIAL_MAX 0
-#endif
-
 #ifndef FF_MIN_STREAK
 #define FF_MIN_STREAK 3
 #endif
@@ -1591,11 +1556,8 @@ __device__ SIM_INLINE void simulate(const Ctx& cx, int64_t ii, const WS& w, int 
                     int b;
                     if (G && __builtin_expect(lut_full, 1)) {
                         int msq;
-                        const int64_t vm = wmin64_redux(v);
-                        b = an <= SCAN_SERIAL_MAX
-                                ? scan_geo<true>(L, geo, rowtab, amask, an, sl, vm, adm, msq, rk_rank, rk_pred, rk_mask, lane)
-                                : scan_geo<false>(L, geo, rowtab, amask, an, sl, vm, adm, msq, rk_rank, rk_pred, rk_mask,
-                                                  lane);
+                        b = scan_geo(L, geo, rowtab, amask, an, sl, wmin64_redux(v), adm, msq, rk_rank, rk_pred,
+                                     rk_mask, lane);
                         ms = msq;
                     } else if (__builtin_expect(lut_full, 1)) {
                         b = scan_slots<G>(L, amask, an, sl, wmin64_redux(v), adm, ms, lane);
