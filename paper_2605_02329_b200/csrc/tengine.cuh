@@ -759,6 +759,7 @@ __device__ __forceinline__ void ldecode_done(St& S, const LWs& w, int64_t t) {
             V0[j * WL] = a; V1[j * WL] = b; AT[j] = tf;
         }
     }
+#ifdef SLOSIM_LANE_LATE_LUT
     if (S.use_lut) {
         // DecodeStepLUT.update on the full power-of-two grid: cell sum/count/mean (slopes follow the means)
         const LGeo& g = S.g;
@@ -773,6 +774,7 @@ __device__ __forceinline__ void ldecode_done(St& S, const LWs& w, int64_t t) {
         C[c] = cnt;
         M[c] = xdiv(sum, (double)cnt);
     }
+#endif
     S.dsteps++;
     uint64_t D = dstep(S.D, (uint64_t)t ^ 0x5A5A5A5A5A5A5A5AULL);
     D = dstep(D, ((uint64_t)hs << 32) | (uint32_t)S.dc_bsz);
@@ -865,6 +867,25 @@ __device__ __forceinline__ void ldecode_start(St& S, const LWs& w, int64_t t) {
     S.dc_bsz = bsz;
     S.dc_max = bmax;
     S.dc_end = t + S.dc_dur;
+#ifndef SLOSIM_LANE_LATE_LUT
+    if (S.use_lut) {
+        // DecodeStepLUT.update (costmodel.py:118-128) of this step's completion, applied as soon as its
+        // ground-truth duration is known: nothing reads the LUT before the next decode start, which
+        // follows the completion, so the state every lookup sees is the reference's.  In the same
+        // block as the ground-truth division, so the two divisions overlap.
+        const LGeo& g = S.g;
+        const int i = min(gbidx(bsz), g.nb - 1);
+        const int j = min(((bmax + (1 << g.wsh) - 1) >> g.wsh) - 1, g.ns - 1);
+        const int c = i * g.ns + j;
+        const auto M = w.mean(), Su = w.sum();
+        const auto C = w.cnt();
+        const double sum = xadd(Su[c], (double)S.dc_dur);
+        const int32_t cnt = C[c] + 1;
+        Su[c] = sum;
+        C[c] = cnt;
+        M[c] = xdiv(sum, (double)cnt);
+    }
+#endif
     LANE_HOOK_DECODE(S, w);
 }
 
