@@ -682,7 +682,7 @@ __device__ __forceinline__ void ldecode_done(St& S, const LWs& w, int64_t t) {
             }
         } else {
 #ifndef SLOSIM_LANE_NO_VBASE
-            if (kairos) vb = min(vb, tf + ((int64_t)(seq - inp) + 1) * S.tpot_slo);
+            vb = min(vb, tf + ((int64_t)(seq - inp) + 1) * S.tpot_slo);
 #endif
             if (o != k) {
                 V0[o * WL] = make_int4(seq, fl, idr, pos);
@@ -781,6 +781,91 @@ __device__ __forceinline__ void ldecode_done(St& S, const LWs& w, int64_t t) {
     S.D = dstep(D, (uint64_t)S.dc_dur);
     S.dc_end = SLOSIM_INF64;
 }
+
+// FCFS-prefill instances fast-forward only once the work queue is drained (the launch's tail, where a
+// lane's latency sets the end): their plain steps are already cheap, and mid-launch the runs cost the
+// warp more than they save (fcfs + continuous alone 299 -> 130M req/s with them, 243M in the tail only)
+#ifdef SLOSIM_LANE_FF_FCFS_ALWAYS
+#define LFF_PREFILL_EXCLUDED(S, tail) false
+#else
+#define LFF_PREFILL_EXCLUDED(S, tail) ((S).ppol == SLOSIM_PREFILL_FCFS && !(tail))
+#endif
+#ifndef SLOSIM_LANE_FF_QUORUM8  // eighths of the live lanes that must be able to fast-forward
+#define SLOSIM_LANE_FF_QUORUM8 5
+#endif
+#ifndef SLOSIM_LANE_FF_MAX
+#define SLOSIM_LANE_FF_MAX 64
+#endif
+// ---- continuous batching (decode_sched.py:114-124) between other events, on the lane.  The step just
+// started batches the whole active set; so does every following decode start until an arrival,
+// transfer or prefill completion (the next rare instant), an admission (which needs one of those or a
+// retirement) or a retirement.  Completions that end before the next rare instant, retire nobody and
+// miss no per-token deadline (metrics.py:57-69) are applied here in step order: the digest fold of
+// each completion, the next step's ground-truth duration (engine.py:185-192) and start.  The step
+// after the run is left in progress for the loop.  The engine's counters and the members' token
+// counts advance by the number of completions.
+#ifndef SLOSIM_LANE_NO_VBASE
+__device__ __forceinline__ void lff_continuous(St& S, const LWs& w) {
+    int64_t tr = min(S.next_arr, S.pf_end);
+    tr = min(tr, S.tr_min);
+    const int an = S.an;
+    const int64_t tpot = S.tpot_slo;
+    // the earliest next-token deadline of the active set (the slack base, kept by the member pass and
+    // admission, less one TPOT): no member misses at completion m iff e_m - (m+1)*tpot <= cmin
+    const int64_t cmin = S.vbase - tpot;  // (lff_ok: the in-progress step's completion is pure)
+    const int4* const V0 = w.v0();
+    const int4* const V1 = w.v1();
+    uint32_t hs = 0;
+    int r = 0x7fffffff;
+    for (int k = 0; k < an; k++) {
+        const int4 a = V0[k * WL], b = V1[k * WL];
+        hs += member_hash((uint32_t)a.w);
+        r = min(r, b.y - 2 - (a.x - b.x));
+    }
+    const uint64_t mid = ((uint64_t)hs << 32) | (uint32_t)an;
+    int m = 0, bmax = S.dc_max;
+    int64_t e = S.dc_end, d = S.dc_dur;
+    uint64_t D = S.D;
+    // completion m: before the next rare instant, nobody retires (m < r), nobody misses a deadline
+    // (e_m - (m+1)*tpot <= tf + n_gen*tpot for every member)
+    // (at most SLOSIM_LANE_FF_MAX per call: a lane alone in a long quiet stretch would otherwise hold
+    // its warp while the other lanes wait at the reconvergence point)
+    const int mmax = min(r, SLOSIM_LANE_FF_MAX);
+    while (m < mmax && e < tr && e - (int64_t)(m + 1) * tpot <= cmin) {
+        D = dstep(D, (uint64_t)e ^ 0x5A5A5A5A5A5A5A5AULL);
+        D = dstep(D, mid);
+        D = dstep(D, (uint64_t)d);
+        m++;
+        bmax++;
+        const double val = S.gline ? gt_line_eval(S.gl, an, bmax)
+                                   : decode_formula(S.P->n_base, S.P->base_x, S.P->base_y, S.P->gamma, an, bmax);
+        d = rint_i64(val);
+        d = d < 1 ? 1 : d;
+        e += d;
+    }
+    if (m == 0) return;
+    const auto AS = w.a32(A_SEQ);
+    for (int k = 0; k < an; k++) AS[k] = AS[k] + m;
+    S.D = D;
+    S.dsteps += m;
+    S.v_dec += (int64_t)m * an;
+    S.b_dec += (int64_t)m * an;
+    S.amax += m;
+    S.dc_max = bmax;
+    S.dc_dur = d;
+    S.dc_end = e;
+}
+
+// A continuous-batching step in progress that batches the whole active set (no admission since its
+// start) and ends before the next rare instant with no member missing its deadline at it.
+__device__ __forceinline__ bool lff_ok(const St& S, bool tail) {
+    if (S.dpol != SLOSIM_DECODE_CONTINUOUS || S.use_lut || S.dc_end == SLOSIM_INF64 || S.dc_prefix != S.an ||
+        S.an < 1 || LFF_PREFILL_EXCLUDED(S, tail))
+        return false;
+    const int64_t tr = min(min(S.next_arr, S.pf_end), S.tr_min);
+    return S.dc_end < tr && S.dc_end <= S.vbase;
+}
+#endif
 
 // ---- start a decode step (engine.py:377-392; decode_sched.py:60-124)
 __device__ __forceinline__ void ldecode_start(St& S, const LWs& w, int64_t t) {
@@ -998,6 +1083,16 @@ __global__ void __launch_bounds__(128, SLOSIM_LANE_MIN_BLOCKS)
             }
         }
         if (live) lstep_c(S, w, t);
+#if !defined(SLOSIM_LANE_NO_FF) && !defined(SLOSIM_LANE_NO_VBASE)
+        // continuous-batching runs are fast-forwarded on the lanes only when (nearly) every live lane of
+        // the warp has one: a lone lane's run would hold the warp while the others wait
+        {
+            const bool drained = __any_sync(FULLMASK, done);  // the work queue is empty (every lane takes part)
+            const bool ffc = live && lff_ok(S, drained);
+            const unsigned cm = __ballot_sync(FULLMASK, ffc), lm = __ballot_sync(FULLMASK, live);
+            if (ffc && __popc(cm) * 8 >= __popc(lm) * SLOSIM_LANE_FF_QUORUM8) lff_continuous(S, w);
+        }
+#endif
         if (__all_sync(FULLMASK, done && !live)) break;
     }
 }

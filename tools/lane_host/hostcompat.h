@@ -53,6 +53,7 @@ static inline unsigned long long atomicAdd(unsigned long long* p, unsigned long 
 template <class T> static inline T __shfl_up_sync(unsigned, T, int) { hc_no_warp(); }
 static inline int __reduce_min_sync(unsigned, int) { hc_no_warp(); }
 static inline int __all_sync(unsigned, int) { hc_no_warp(); }
+static inline int __any_sync(unsigned, int) { hc_no_warp(); }
 
 // CUDA's vector types (the lane engine's active-set entries)
 struct alignas(16) int4 { int x, y, z, w; };
