@@ -782,16 +782,17 @@ __device__ __forceinline__ void ldecode_done(St& S, const LWs& w, int64_t t) {
     S.dc_end = SLOSIM_INF64;
 }
 
-// FCFS-prefill instances fast-forward only once the work queue is drained (the launch's tail, where a
-// lane's latency sets the end): their plain steps are already cheap, and mid-launch the runs cost the
-// warp more than they save (fcfs + continuous alone 299 -> 130M req/s with them, 243M in the tail only)
-#ifdef SLOSIM_LANE_FF_FCFS_ALWAYS
-#define LFF_PREFILL_EXCLUDED(S, tail) false
-#else
+// FCFS-prefill instances fast-forward at every trip by default.  Alone, fcfs + continuous is faster with
+// its runs confined to the launch's tail (299 -> 130M req/s with them everywhere, 243M in the tail only),
+// but in the config-5 mix the warp's other lanes gain more than it loses: on 131,072-instance slices
+// 48.4M (tail only, quorum 5/8) -> 50.6-51.3M req/s (always, quorum 1/8), `profiles/r2p_ff_quorum_ab.log`.
+#ifdef SLOSIM_LANE_FF_FCFS_TAIL_ONLY
 #define LFF_PREFILL_EXCLUDED(S, tail) ((S).ppol == SLOSIM_PREFILL_FCFS && !(tail))
+#else
+#define LFF_PREFILL_EXCLUDED(S, tail) false
 #endif
 #ifndef SLOSIM_LANE_FF_QUORUM8  // eighths of the live lanes that must be able to fast-forward
-#define SLOSIM_LANE_FF_QUORUM8 5
+#define SLOSIM_LANE_FF_QUORUM8 1
 #endif
 #ifndef SLOSIM_LANE_FF_MAX
 #define SLOSIM_LANE_FF_MAX 64
